@@ -1,0 +1,119 @@
+/*
+ * eik_ifim.h -- C ABI of the B200 iFIM engine (libeik_ifim.so).
+ *
+ * Drop-in boundary for the reference's iFIM path.  The reference is a Python
+ * package (`eikonal`, /root/reference/pkg/src/eikonal = E/) with no native
+ * code; its "operator API" for this path is the Python solver signature
+ * family, which paper_2106_15869_b200/ifim.py keeps and binds to these entry
+ * points through ctypes (see INTEGRATION.md for the binding a maintainer of
+ * the reference would add).
+ *
+ *   eik_ifim_update_step  replaces ifim_update_step  (E/ifim.py:75-134)
+ *   eik_build_remedy      replaces build_remedy_set  (E/ifim.py:137-161)
+ *   eik_remedy_step       replaces ifim_remedy_step  (E/ifim.py:164-218)
+ *   eik_ifim_solve        replaces solve_ifim        (E/ifim.py:221-235)
+ *   eik_remedy_load / eik_remedy_export
+ *                         replace RemedySet's member mask (E/ifim.py:64-72)
+ *   eik_local_solve       replaces update_batch / update_3d_uniform
+ *                         (E/_kernels.py:41-88, E/local_solver.py:91-157)
+ *
+ * Conventions (E/grid.py:1-8, 21-26): phi float64 with +inf = unreached,
+ * speed float64 >= 0 (0 = Blocked), state uint8 CellState codes
+ * {FAR 0, ACTIVE 1, SOURCE 2, REMEDY 3, BLOCKED 4}; linear index j*nx+i in 2D
+ * and (k*ny+j)*nx+i in 3D.  All array pointers are DEVICE pointers; `stream`
+ * is a cudaStream_t passed as void*.  Every function returns an int status
+ * (EIK_OK ...); the message of the last failure on the calling thread is
+ * available from eik_last_error().  The caller allocates the workspace
+ * (eik_workspace_size); the library allocates nothing persistently.  Calls
+ * block until their statistics are on the host.
+ */
+#ifndef EIK_IFIM_H
+#define EIK_IFIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EIK_OK 0
+#define EIK_EINVAL 1 /* -> ValueError   (E/ifim.py:83-84, E/grid.py:204-211) */
+#define EIK_ECAP 2   /* -> RuntimeError (E/ifim.py:109-110, 188-189) */
+#define EIK_ECUDA 3
+#define EIK_ENCCL 4
+
+#define EIK_F64 0
+
+typedef struct eik_geom {
+    int64_t nx, ny, nz; /* nz = 1 for 2D */
+    double dx, dy, dz;  /* 3D requires dx == dy == dz */
+    int32_t ndim;       /* 2 or 3 */
+    int32_t dtype;      /* EIK_F64 */
+} eik_geom;
+
+/* RunStats (E/result.py:9-18) plus device-side extras. */
+typedef struct eik_stats {
+    int64_t iterations;   /* update iterations + remedy rounds */
+    int64_t solver_calls; /* local-solver invocations (node updates) */
+    int64_t peak_active;
+    int64_t peak_remedy;
+    int64_t phi_writes;   /* non-converged update writes + remedy decreases */
+    int64_t history_len;  /* entries written to the active_history buffer */
+    int64_t remedy_size;  /* cells flagged by the build pass */
+    int64_t converged;    /* cells labelled CONVERGED by the update step */
+    int64_t upd_iterations, upd_calls, build_calls, rem_iterations, rem_calls;
+    int64_t gpu_launches; /* kernels launched by this call */
+    float upd_ms, build_ms, rem_ms, total_ms; /* device time (CUDA events) */
+} eik_stats;
+
+/* Bytes of device workspace needed for a grid. */
+int eik_workspace_size(const eik_geom *g, size_t *bytes);
+
+/* Update step (E/ifim.py:75-134).  Applies the seeds first (E/grid.py:212-215:
+ * phi[seed] = value, state[seed] = SOURCE); seed_idx/seed_val are device
+ * arrays of nseeds linear indices and values, validated by the caller.
+ * history (HOST, int64[history_cap]) receives active_history. */
+int eik_ifim_update_step(const eik_geom *g, double *phi, const double *speed, uint8_t *state,
+                         const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
+                         void *workspace, size_t workspace_bytes, int64_t *history,
+                         int64_t history_cap, eik_stats *out, void *stream);
+
+/* Build pass (E/ifim.py:137-161).  Leaves the remedy set in the workspace;
+ * out->remedy_size = |R0|, out->solver_calls = #free cells. */
+int eik_build_remedy(const eik_geom *g, const double *phi, const double *speed, const uint8_t *state,
+                     double tol, void *workspace, size_t workspace_bytes, eik_stats *out, void *stream);
+
+/* Load a remedy set from a device bool/uint8 mask[N] (a RemedySet built elsewhere). */
+int eik_remedy_load(const eik_geom *g, const uint8_t *member, const uint8_t *state, void *workspace,
+                    size_t workspace_bytes, int64_t *count, void *stream);
+
+/* Write the workspace remedy set as a device uint8 mask[N]. */
+int eik_remedy_export(const eik_geom *g, void *workspace, size_t workspace_bytes, uint8_t *member,
+                      void *stream);
+
+/* Remedy step (E/ifim.py:164-218) on the workspace remedy set; drains it. */
+int eik_remedy_step(const eik_geom *g, double *phi, const double *speed, const uint8_t *state,
+                    double tol, void *workspace, size_t workspace_bytes, eik_stats *out, void *stream);
+
+/* solve_ifim (E/ifim.py:221-235): update step + build + remedy, device-resident,
+ * one host synchronisation at the end. */
+int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t *state,
+                   const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
+                   void *workspace, size_t workspace_bytes, int64_t *history, int64_t history_cap,
+                   eik_stats *out, void *stream);
+
+/* Element-wise local solver on device arrays (parity hook for
+ * E/_kernels.py:41-88 and E/local_solver.py:91-157).  kind: 0 = 2D uniform
+ * (a, b, f, dx), 1 = 2D anisotropic (a, b, f, dx, dy), 2 = 3D uniform
+ * (a, b, c, f, dx). */
+int eik_local_solve(int kind, const double *a, const double *b, const double *c, const double *f,
+                    double dx, double dy, double *out, int64_t n, void *stream);
+
+const char *eik_last_error(void);
+const char *eik_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EIK_IFIM_H */

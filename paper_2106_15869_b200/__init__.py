@@ -1,0 +1,42 @@
+"""B200-native iFIM (improved fast iterative method, arXiv 2106.15869).
+
+Drop-in for the reference package's iFIM path (``eikonal.solve_ifim`` and the
+staged ``ifim_update_step`` / ``build_remedy_set`` / ``ifim_remedy_step``),
+with the reference's grid / speed / source / result conventions, extended to
+3D cubic grids.  All solving happens in hand-written sm_100a CUDA kernels
+behind the C ABI in include/eik_ifim.h; there is no CPU fallback.
+"""
+from .grid import (
+    INF,
+    BoundaryCondition,
+    CellIndex,
+    CellIndex3D,
+    CellState,
+    Grid,
+    Grid3D,
+    new_grid,
+    new_grid_3d,
+    reset_field,
+    seed_linear,
+    seed_point,
+)
+from .harness import METHOD_NAMES, PARALLEL_METHODS, field_max_diff, field_sha256, run_method
+from .ifim import (
+    RemedySet,
+    build_remedy_set,
+    clear_workspaces,
+    ifim_remedy_step,
+    ifim_update_step,
+    resolve_workers,
+    solve_ifim,
+)
+from .result import RunStats, SolverResult
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "INF", "BoundaryCondition", "CellIndex", "CellIndex3D", "CellState", "Grid", "Grid3D", "METHOD_NAMES",
+    "PARALLEL_METHODS", "RemedySet", "RunStats", "SolverResult", "build_remedy_set", "clear_workspaces",
+    "field_max_diff", "field_sha256", "ifim_remedy_step", "ifim_update_step", "new_grid", "new_grid_3d",
+    "reset_field", "resolve_workers", "run_method", "seed_linear", "seed_point", "solve_ifim",
+]

@@ -1,0 +1,1362 @@
+// eik_ifim.cu -- B200 (sm_100a) engine for the improved fast iterative method.
+//
+// Implements the C ABI declared in include/eik_ifim.h.  The reference path it
+// replaces is E/ifim.py (E = /root/reference/pkg/src/eikonal):
+//
+//   update step  (E/ifim.py:75-134)  -> k_update   persistent, push/worklist
+//   build pass   (E/ifim.py:137-161) -> k_build    one streaming pass
+//   remedy step  (E/ifim.py:164-218) -> k_remedy   persistent, pull/bitmap
+//
+// Data layout in HBM:
+//   * phi: the caller's float64 array (row-major, x fastest) plus one
+//     workspace copy.  The two form a Jacobi double buffer: iteration k reads
+//     P[k&1] and every processed cell writes its final value into P[(k+1)&1],
+//     which keeps the snapshot semantics of padded_phi (E/_kernels.py:21-26)
+//     without any O(N) copy per iteration.  At termination both are equal.
+//   * d = delta / F precomputed per cell (bit-identical to the per-call
+//     division at E/_kernels.py:48 and E/local_solver.py:105).
+//   * Sets are bitmaps with one 32-bit word per 32 consecutive cells of one
+//     x-row (word w <-> row w / W, lanes x = 32*(w % W) + lane); a warp owns a
+//     word, lane = cell.  Rows are padded to whole words.
+//   * Worklists are compacted lists of non-empty words.
+//
+// Arithmetic is float64 IEEE with FMA contraction disabled (-fmad=false) and
+// the reference's operation order, so phi is bit-identical to the reference
+// and every RunStats integer (iterations, solver_calls, peaks, active_history)
+// matches exactly.
+//
+// Termination is device-side: the persistent kernels loop over iterations
+// with a software grid barrier (co-residency guaranteed by a cooperative
+// launch) and read the global set size after each barrier; the host sees only
+// the final statistics.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "eik_ifim.h"
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int BLOCK = 256;
+constexpr int WPB = BLOCK / 32;
+constexpr int APPBUF = 64;  // per-warp append buffer (entries)
+constexpr uint8_t ST_SOURCE = 2, ST_BLOCKED = 4;  // E/grid.py:21-26
+enum { SOL_U2 = 0, SOL_A2 = 1, SOL_U3 = 2 };
+
+// E/_kernels.py:18 (math.sqrt(2.0)) and E/local_solver.py:28
+__device__ __constant__ double kSqrt2 = 1.4142135623730951;
+#define DISC_CLAMP 1e-12
+
+struct Ctl {
+    unsigned bar_count;
+    unsigned bar_gen;
+    unsigned len[3];
+    unsigned err;
+    unsigned long long cnt[3];
+    unsigned long long sum;     // sum of set sizes over iterations (solver calls)
+    unsigned long long peak;    // peak set size
+    unsigned long long writes;  // phi writes
+    unsigned long long conv;    // cells converged (update)
+    unsigned long long iters;   // iterations / rounds executed
+    unsigned long long free_cells;  // build: #free
+    unsigned long long flagged;     // build: |R0|
+    unsigned long long pad[3];
+};
+
+struct KP {
+    int64_t nx, ny, nz, plane;
+    uint32_t W, nwords, nrows, pad0;
+    double dx, dy, delta, tol;
+    double *P0, *P1;         // P0 = caller phi, P1 = workspace copy
+    const double *F;         // speed
+    double *dd;              // delta / F (uniform solvers)
+    const uint8_t *state;
+    uint32_t *B0, *B1, *Bt, *Bf;  // bitmaps: set A/B, touched, fixed (blocked|source)
+    uint32_t *L0, *L1;            // worklists (uint32 words or uint2 entries)
+    Ctl *ctl;
+    int64_t *hist;
+    int64_t hist_cap;
+    int64_t cap;
+};
+
+// ---------------------------------------------------------------------------
+// Local solvers (bit-exact restatements; no FMA contraction)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double dmin(double a, double b) { return a <= b ? a : b; }
+__device__ __forceinline__ double dmax(double a, double b) { return a >= b ? a : b; }
+// numpy.maximum(x, 0.0): NaN propagates
+__device__ __forceinline__ double npmax0(double x) { return (x != x) ? x : (x >= 0.0 ? x : 0.0); }
+
+// E/_kernels.py:47-58 (_update_uniform_batch), d = delta / f
+__device__ __forceinline__ double upd2u(double a, double b, double d)
+{
+    const double lo = dmin(a, b);
+    const double hi = dmax(a, b);
+    const double one = lo + d;
+    const double diff = hi - lo;
+    const bool take_two = diff <= kSqrt2 * d;
+    const double disc = 2.0 * d * d - diff * diff;
+    const double root = 0.5 * (a + b + sqrt(npmax0(disc)));
+    const bool valid = take_two && (disc >= -DISC_CLAMP * (2.0 * d * d)) && (root >= hi);
+    return valid ? root : one;
+}
+
+// E/_kernels.py:61-88 (_update_aniso_batch)
+__device__ __forceinline__ double upd2a(double a, double b, double f, double dx, double dy)
+{
+    const double one_x = a + dx / f;
+    const double one_y = b + dy / f;
+    const double dx2 = dx * dx;
+    const double dy2 = dy * dy;
+    const double s2 = (dx2 + dy2) / (f * f);
+    const double s = sqrt(s2);
+    const double diff = a - b;
+    const double disc = s2 - diff * diff;
+    const double root = (a * dy2 + b * dx2 + (dx * dy) * sqrt(npmax0(disc))) / (dx2 + dy2);
+    const double drop_larger = (a > b) ? one_y : one_x;
+    const bool valid = isfinite(a) && isfinite(b) && !(diff > s) && !(-diff > s) &&
+                       (disc >= -DISC_CLAMP * s2) && (root >= a) && (root >= b);
+    double out = valid ? root : drop_larger;
+    if (isinf(a) && isfinite(b)) out = one_y;
+    if (isfinite(a) && isinf(b)) out = one_x;
+    if (isinf(a) && isinf(b)) out = INFINITY;
+    return out;
+}
+
+// E/local_solver.py:91-157 (update_3d_uniform), verified branch walk; d = delta / f
+__device__ __forceinline__ double upd3u(double px, double py, double pz, double d, double delta)
+{
+    double a1 = px, a2 = py, a3 = pz, t;
+    if (a2 < a1) { t = a1; a1 = a2; a2 = t; }
+    if (a3 < a2) { t = a2; a2 = a3; a3 = t; }
+    if (a2 < a1) { t = a1; a1 = a2; a2 = t; }
+    if (a1 == INFINITY) return INFINITY;
+    int k = (a3 - a1 < delta) ? 3 : ((a2 - a1 < delta) ? 2 : 1);
+    unsigned visited = 0;
+#pragma unroll 1
+    for (int guard = 0; guard < 8; ++guard) {
+        visited |= 1u << k;
+        if (k == 3) {
+            const double b2 = a2 - a1;
+            const double b3 = a3 - a1;
+            const double s = b2 + b3;
+            const double disc = s * s - 3.0 * (b2 * b2 + b3 * b3 - d * d);
+            if (disc < -DISC_CLAMP * (3.0 * d * d)) { k = 2; continue; }
+            const double root = a1 + (s + sqrt(disc > 0.0 ? disc : 0.0)) / 3.0;
+            if (root >= a3 || (visited & 4u)) return root;
+            k = 2;
+        } else if (k == 2) {
+            if (a2 == INFINITY) { k = 1; continue; }
+            const double diff = a2 - a1;
+            const double disc = 2.0 * d * d - diff * diff;
+            if (disc < -DISC_CLAMP * (2.0 * d * d)) { k = 1; continue; }
+            const double root = 0.5 * (a1 + a2 + sqrt(disc > 0.0 ? disc : 0.0));
+            if (root < a2 && !(visited & 2u)) { k = 1; continue; }
+            if (root > a3 && !(visited & 8u)) { k = 3; continue; }
+            return root;
+        } else {
+            const double root = a1 + d;
+            if (root > a2 && !(visited & 4u)) { k = 2; continue; }
+            return root;
+        }
+    }
+    return NAN;  // unreachable: the walk visits each branch at most twice
+}
+
+// ---------------------------------------------------------------------------
+// small helpers
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
+__device__ __forceinline__ uint32_t ldcg(const uint32_t *p) { return __ldcg(p); }
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
+
+template <typename T>
+__device__ __forceinline__ T vload(const T *p) { return *(const volatile T *)p; }
+
+// Software grid barrier; all CTAs are co-resident (cooperative launch).
+__device__ __forceinline__ void grid_barrier(Ctl *ctl)
+{
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *vgen = &ctl->bar_gen;
+        const unsigned gen = *vgen;
+        __threadfence();
+        const unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
+        if (arrived == gridDim.x - 1) {
+            atomicExch(&ctl->bar_count, 0u);
+            __threadfence();
+            atomicAdd(&ctl->bar_gen, 1u);
+        } else {
+            while (*vgen == gen) { __nanosleep(32); }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+// Sum a per-thread value over the block; result valid in thread 0.
+__device__ __forceinline__ unsigned long long block_sum(unsigned long long v, unsigned long long *sm)
+{
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane_id() == 0) sm[w] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < WPB; ++i) t += sm[i];
+    __syncthreads();
+    return t;
+}
+
+struct WPos {
+    uint32_t row, wx, y, z;
+    int64_t x0, c0;
+    uint32_t rowm;  // lanes inside the row
+};
+
+template <int DIM>
+__device__ __forceinline__ WPos wpos(const KP &p, uint32_t w)
+{
+    WPos q;
+    q.row = w / p.W;
+    q.wx = w - q.row * p.W;
+    if (DIM == 3) {
+        q.z = q.row / (uint32_t)p.ny;
+        q.y = q.row - q.z * (uint32_t)p.ny;
+    } else {
+        q.z = 0;
+        q.y = q.row;
+    }
+    q.x0 = (int64_t)q.wx * 32;
+    q.c0 = (int64_t)q.row * p.nx + q.x0;
+    const int64_t nv = p.nx - q.x0;
+    q.rowm = nv >= 32 ? FULL : ((1u << nv) - 1u);
+    return q;
+}
+
+struct Sten {
+    double c, w, e, s, n, d, u;
+};
+
+// Gather the Jacobi snapshot around the lanes in `bits` (E/_kernels.py:29-38:
+// out-of-grid reads are +inf).  Lanes adjacent to an active lane also load
+// their own value so x-neighbours come from shuffles.
+template <int DIM>
+__device__ __forceinline__ void gather(const KP &p, const double *__restrict__ Pc, const WPos &q, uint32_t bits,
+                                       Sten &s)
+{
+    const unsigned lane = lane_id();
+    const bool act = (bits >> lane) & 1u;
+    const uint32_t need = (bits | (bits << 1) | (bits >> 1)) & q.rowm;
+    const int64_t c = q.c0 + lane;
+    s.c = ((need >> lane) & 1u) ? ldcg(Pc + c) : INFINITY;
+    double w = __shfl_up_sync(FULL, s.c, 1);
+    double e = __shfl_down_sync(FULL, s.c, 1);
+    if (lane == 0) w = (act && q.wx > 0) ? ldcg(Pc + c - 1) : INFINITY;
+    if (lane == 31) e = (act && q.x0 + 32 < p.nx) ? ldcg(Pc + c + 1) : INFINITY;
+    else if (q.x0 + lane + 1 >= p.nx) e = INFINITY;
+    s.w = w;
+    s.e = e;
+    s.s = s.n = s.d = s.u = INFINITY;
+    if (act) {
+        if (q.y > 0) s.s = ldcg(Pc + c - p.nx);
+        if (q.y + 1 < p.ny) s.n = ldcg(Pc + c + p.nx);
+        if (DIM == 3) {
+            if (q.z > 0) s.d = ldcg(Pc + c - p.plane);
+            if (q.z + 1 < p.nz) s.u = ldcg(Pc + c + p.plane);
+        }
+    }
+}
+
+// One local-solver call on the gathered stencil (E/ifim.py:57-59).
+template <int DIM, int SOL>
+__device__ __forceinline__ double solve(const KP &p, const Sten &s, int64_t c)
+{
+    const double xm = dmin(s.w, s.e);
+    const double ym = dmin(s.s, s.n);
+    if (SOL == SOL_U2) return upd2u(xm, ym, __ldg(p.dd + c));
+    if (SOL == SOL_A2) return upd2a(xm, ym, __ldg(p.F + c), p.dx, p.dy);
+    return upd3u(xm, ym, dmin(s.d, s.u), __ldg(p.dd + c), p.delta);
+}
+
+// Per-warp append buffer in shared memory -> global worklist.
+struct Appender {
+    uint32_t *buf;  // APPBUF entries (shared)
+    int n;          // warp-uniform fill
+};
+
+__device__ __forceinline__ void app_flush(Appender &a, uint32_t *glist, unsigned *glen)
+{
+    __syncwarp();
+    if (a.n == 0) return;
+    unsigned base = 0;
+    if (lane_id() == 0) base = atomicAdd(glen, (unsigned)a.n);
+    base = __shfl_sync(FULL, base, 0);
+    for (int i = lane_id(); i < a.n; i += 32) glist[base + i] = a.buf[i];
+    __syncwarp();
+    a.n = 0;
+}
+
+__device__ __forceinline__ void app_push(Appender &a, bool want, uint32_t val, uint32_t *glist, unsigned *glen)
+{
+    const unsigned m = __ballot_sync(FULL, want);
+    if (want) a.buf[a.n + __popc(m & lanemask_lt())] = val;
+    a.n += __popc(m);
+    if (a.n > APPBUF - 32) app_flush(a, glist, glen);
+}
+
+// ---------------------------------------------------------------------------
+// Preparation kernels
+// ---------------------------------------------------------------------------
+
+// apply_boundary writes (E/grid.py:212-215); validation is done by the caller.
+__global__ void k_seed(double *phi, uint8_t *state, const int64_t *idx, const double *val, int64_t n)
+{
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        phi[idx[s]] = val[s];
+        state[idx[s]] = ST_SOURCE;
+    }
+}
+
+// One pass over all words: copy phi into the second buffer, d = delta / F,
+// touched = blocked, fixed = blocked | source, optionally clear set bitmaps.
+template <bool UNIFORM>
+__global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_touched, uint32_t *clr0,
+                                                uint32_t *clr1)
+{
+    const unsigned lane = lane_id();
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t w = gw; w < p.nwords; w += GW) {
+        const uint32_t row = w / p.W;
+        const int64_t x = (int64_t)(w - row * p.W) * 32 + lane;
+        const bool in = x < p.nx;
+        const int64_t c = (int64_t)row * p.nx + x;
+        uint8_t st = 0;
+        if (in) {
+            st = p.state[c];
+            if (copy_phi) p.P1[c] = p.P0[c];
+            if (UNIFORM) p.dd[c] = p.delta / p.F[c];
+        }
+        const uint32_t blk = __ballot_sync(FULL, in && st == ST_BLOCKED);
+        const uint32_t src = __ballot_sync(FULL, in && st == ST_SOURCE);
+        if (lane == 0) {
+            p.Bf[w] = blk | src;
+            if (build_touched) p.Bt[w] = blk;
+            if (clr0) clr0[w] = 0;
+            if (clr1) clr1[w] = 0;
+        }
+    }
+}
+
+// Initial Active = free FAR axis neighbours of the seeds (E/ifim.py:97-102).
+template <int DIM>
+__global__ void k_init_active(KP p, const int64_t *seeds, int64_t nseeds)
+{
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseeds; s += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = seeds[s];
+        const int64_t i = c % p.nx;
+        const int64_t r = c / p.nx;
+        const int64_t j = r % p.ny;
+        const int64_t k = r / p.ny;
+        int64_t nb[6];
+        int m = 0;
+        if (i > 0) nb[m++] = c - 1;
+        if (i < p.nx - 1) nb[m++] = c + 1;
+        if (j > 0) nb[m++] = c - p.nx;
+        if (j < p.ny - 1) nb[m++] = c + p.nx;
+        if (DIM == 3) {
+            if (k > 0) nb[m++] = c - p.plane;
+            if (k < p.nz - 1) nb[m++] = c + p.plane;
+        }
+        for (int t = 0; t < m; ++t) {
+            const int64_t e = nb[t];
+            const uint8_t st = p.state[e];
+            if (st == ST_BLOCKED || st == ST_SOURCE) continue;
+            const int64_t row = e / p.nx;
+            const int64_t x = e - row * p.nx;
+            const uint32_t w = (uint32_t)(row * p.W + (x >> 5));
+            const uint32_t bit = 1u << (x & 31);
+            const uint32_t old = atomicOr(p.Bt + w, bit);
+            if (old & bit) continue;  // label != FAR
+            const uint32_t olda = atomicOr(p.B0 + w, bit);
+            if (olda == 0) p.L0[atomicAdd(&p.ctl->len[0], 1u)] = w;
+            atomicAdd(&p.ctl->cnt[0], 1ull);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Update step: persistent kernel, one iteration per grid barrier
+// ---------------------------------------------------------------------------
+
+template <int DIM, int SOL>
+__device__ __forceinline__ void upd_word(const KP &p, uint32_t w, const double *__restrict__ Pc, double *__restrict__ Pn,
+                                         uint32_t *Ac, uint32_t *An, uint32_t *Ln, unsigned *lenN, Appender &app,
+                                         unsigned long long &a_next, unsigned long long &a_writes,
+                                         unsigned long long &a_conv)
+{
+    const unsigned lane = lane_id();
+    const uint32_t bits = ldcg(Ac + w);
+    __syncwarp();
+    if (lane == 0) Ac[w] = 0;  // consumed; this bitmap is the next-next one
+    const WPos q = wpos<DIM>(p, w);
+    Sten s;
+    gather<DIM>(p, Pc, q, bits, s);
+    const bool act = (bits >> lane) & 1u;
+    const int64_t c = q.c0 + lane;
+    double v = 0.0;
+    if (act) v = solve<DIM, SOL>(p, s, c);
+    // E/ifim.py:121: converged iff v == old or |v - old| <= tol
+    const bool conv = act && (v == s.c || fabs(v - s.c) <= p.tol);
+    const bool stay = act && !conv;
+    if (act) Pn[c] = stay ? v : s.c;  // E/ifim.py:128 (+ double-buffer carry)
+    const uint32_t stay_m = __ballot_sync(FULL, stay);
+    const uint32_t conv_m = __ballot_sync(FULL, conv);
+    if (lane == 0) {
+        a_writes += __popc(stay_m);
+        a_conv += __popc(conv_m);
+    }
+    // Activation of +inf, unblocked, FAR neighbours of converged cells (E/ifim.py:123-126).
+    const uint32_t inf_m = __ballot_sync(FULL, s.c == INFINITY);
+    const bool wcand = __ballot_sync(FULL, lane == 0 && conv && q.wx > 0 && s.w == INFINITY) != 0;
+    const bool ecand = __ballot_sync(FULL, lane == 31 && conv && q.x0 + 32 < p.nx && s.e == INFINITY) != 0;
+    const uint32_t cs = (q.y > 0) ? (conv_m & __ballot_sync(FULL, s.s == INFINITY)) : 0u;
+    const uint32_t cn = (q.y + 1 < p.ny) ? (conv_m & __ballot_sync(FULL, s.n == INFINITY)) : 0u;
+    uint32_t cd = 0, cu = 0;
+    if (DIM == 3) {
+        cd = (q.z > 0) ? (conv_m & __ballot_sync(FULL, s.d == INFINITY)) : 0u;
+        cu = (q.z + 1 < p.nz) ? (conv_m & __ballot_sync(FULL, s.u == INFINITY)) : 0u;
+    }
+    uint32_t cand = 0, extra = 0, tw = 0;
+    switch (lane) {
+        case 0: tw = w; cand = ((conv_m << 1) | (conv_m >> 1)) & inf_m & q.rowm; extra = stay_m; break;
+        case 1: tw = w - 1; cand = wcand ? 0x80000000u : 0u; break;
+        case 2: tw = w + 1; cand = ecand ? 1u : 0u; break;
+        case 3: tw = w - p.W; cand = cs; break;
+        case 4: tw = w + p.W; cand = cn; break;
+        case 5: tw = (uint32_t)(w - (uint32_t)p.ny * p.W); cand = cd; break;
+        case 6: tw = (uint32_t)(w + (uint32_t)p.ny * p.W); cand = cu; break;
+        default: break;
+    }
+    bool want = false;
+    if (cand | extra) {
+        uint32_t nb = 0;
+        if (cand) {
+            const uint32_t old = atomicOr(p.Bt + tw, cand);  // FAR -> ACTIVE exactly once
+            nb = cand & ~old;
+        }
+        const uint32_t setm = nb | extra;
+        if (setm) {
+            const uint32_t olda = atomicOr(An + tw, setm);
+            a_next += __popc(setm & ~olda);
+            want = (olda == 0);
+        }
+    }
+    app_push(app, want, tw, Ln, lenN);
+}
+
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK) k_update(KP p)
+{
+    __shared__ uint32_t sbuf[WPB][APPBUF];
+    __shared__ unsigned long long sred[WPB];
+    const unsigned warp = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * WPB + warp;
+    const uint32_t GW = gridDim.x * WPB;
+    Ctl *ctl = p.ctl;
+    Appender app{sbuf[warp], 0};
+    unsigned long long a_writes = 0, a_conv = 0;
+
+    const unsigned long long n0 = vload(&ctl->cnt[0]);
+    if (n0 == 0) return;  // no initial active cell: zero iterations
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (p.hist_cap > 0) p.hist[0] = (int64_t)n0;
+        ctl->sum = n0;
+        ctl->peak = n0;
+    }
+    for (int64_t it = 0;; ++it) {
+        const int par = (int)(it & 1);
+        const double *Pc = par ? p.P1 : p.P0;
+        double *Pn = par ? p.P0 : p.P1;
+        uint32_t *Ac = par ? p.B1 : p.B0;
+        uint32_t *An = par ? p.B0 : p.B1;
+        const uint32_t *Lc = par ? p.L1 : p.L0;
+        uint32_t *Ln = par ? p.L0 : p.L1;
+        unsigned *lenN = &ctl->len[(it + 1) % 3];
+        const unsigned n = vload(&ctl->len[it % 3]);
+        unsigned long long a_next = 0;
+        for (uint32_t i = gw; i < n; i += GW)
+            upd_word<DIM, SOL>(p, ldcg(Lc + i), Pc, Pn, Ac, An, Ln, lenN, app, a_next, a_writes, a_conv);
+        app_flush(app, Ln, lenN);
+        const unsigned long long tot = block_sum(a_next, sred);
+        if (threadIdx.x == 0) {
+            if (tot) atomicAdd(&ctl->cnt[(it + 1) % 3], tot);
+            if (blockIdx.x == 0) {
+                ctl->len[(it + 2) % 3] = 0;
+                ctl->cnt[(it + 2) % 3] = 0;
+            }
+        }
+        grid_barrier(ctl);
+        const unsigned long long m = vload(&ctl->cnt[(it + 1) % 3]);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctl->iters = it + 1;
+            if (m) {
+                if (it + 1 < p.hist_cap) p.hist[it + 1] = (int64_t)m;
+                ctl->sum += m;
+                if (m > ctl->peak) ctl->peak = m;
+            }
+        }
+        if (m == 0) break;
+        if (it + 1 >= p.cap) {  // E/ifim.py:106-110
+            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
+            break;
+        }
+    }
+    const unsigned long long tw = block_sum(a_writes, sred);
+    const unsigned long long tc = block_sum(a_conv, sred);
+    if (threadIdx.x == 0) {
+        atomicAdd(&ctl->writes, tw);
+        atomicAdd(&ctl->conv, tc);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Build pass (E/ifim.py:137-161): one value per free cell, flag |v - phi| > tol.
+// Writes the remedy list R0 as (word, bits) entries and zeroes D[0].
+// ---------------------------------------------------------------------------
+
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK) k_build(KP p, const double *__restrict__ Pc, uint2 *E0, uint32_t *D0,
+                                                 const unsigned *skip)
+{
+    __shared__ uint32_t sbuf[WPB][APPBUF];
+    __shared__ uint32_t sbits[WPB][APPBUF];
+    __shared__ unsigned long long sred[WPB];
+    if (skip && *skip) return;
+    const unsigned lane = lane_id();
+    const unsigned warp = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * WPB + warp;
+    const uint32_t GW = gridDim.x * WPB;
+    Ctl *ctl = p.ctl;
+    int nb = 0;
+    unsigned long long a_free = 0, a_flag = 0;
+    for (uint32_t w = gw; w < p.nwords; w += GW) {
+        const WPos q = wpos<DIM>(p, w);
+        const uint32_t freem = q.rowm & ~__ldg(p.Bf + w);
+        if (lane == 0) D0[w] = 0;
+        if (freem == 0) continue;
+        Sten s;
+        gather<DIM>(p, Pc, q, freem, s);
+        const bool fr = (freem >> lane) & 1u;
+        bool moved = false;
+        if (fr) {
+            const double v = solve<DIM, SOL>(p, s, q.c0 + lane);
+            moved = fabs(v - s.c) > p.tol;  // NaN (inf - inf) is not flagged
+        }
+        const uint32_t mm = __ballot_sync(FULL, moved);
+        if (lane == 0) {
+            a_free += __popc(freem);
+            a_flag += __popc(mm);
+        }
+        if (mm) {
+            if (lane == 0) {
+                sbuf[warp][nb] = w;
+                sbits[warp][nb] = mm;
+            }
+            ++nb;
+            if (nb == APPBUF) {
+                __syncwarp();
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(&ctl->len[0], (unsigned)nb);
+                base = __shfl_sync(FULL, base, 0);
+                for (int i = lane; i < nb; i += 32) E0[base + i] = make_uint2(sbuf[warp][i], sbits[warp][i]);
+                __syncwarp();
+                nb = 0;
+            }
+        }
+    }
+    __syncwarp();
+    if (nb) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(&ctl->len[0], (unsigned)nb);
+        base = __shfl_sync(FULL, base, 0);
+        for (int i = lane; i < nb; i += 32) E0[base + i] = make_uint2(sbuf[warp][i], sbits[warp][i]);
+    }
+    const unsigned long long tf = block_sum(a_free, sred);
+    const unsigned long long tg = block_sum(a_flag, sred);
+    if (threadIdx.x == 0) {
+        atomicAdd(&ctl->free_cells, tf);
+        atomicAdd(&ctl->flagged, tg);
+        atomicAdd(&ctl->cnt[0], tg);
+    }
+}
+
+// Remedy set from a uint8 mask (RemedySet.member), zeroing D[0].
+__global__ void __launch_bounds__(BLOCK) k_remedy_load(KP p, const uint8_t *member, uint2 *E0, uint32_t *D0)
+{
+    const unsigned lane = lane_id();
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
+    unsigned long long cnt = 0;
+    for (uint32_t w = gw; w < p.nwords; w += GW) {
+        const uint32_t row = w / p.W;
+        const int64_t x = (int64_t)(w - row * p.W) * 32 + lane;
+        const bool in = x < p.nx;
+        const int64_t c = (int64_t)row * p.nx + x;
+        const uint32_t m = __ballot_sync(FULL, in && member[c] != 0);
+        if (lane == 0) {
+            D0[w] = 0;
+            if (m) {
+                E0[atomicAdd(&p.ctl->len[0], 1u)] = make_uint2(w, m);
+                cnt += __popc(m);
+            }
+        }
+    }
+    if (lane == 0 && cnt) atomicAdd(&p.ctl->cnt[0], cnt);
+}
+
+__global__ void k_remedy_export(KP p, const uint2 *E0, unsigned n, uint8_t *member)
+{
+    const unsigned lane = lane_id();
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t i = gw; i < n; i += GW) {
+        const uint2 e = E0[i];
+        const uint32_t row = e.x / p.W;
+        const int64_t x = (int64_t)(e.x - row * p.W) * 32 + lane;
+        if ((e.y >> lane) & 1u) member[(int64_t)row * p.nx + x] = 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Remedy step: persistent kernel, two phases per round.
+//   A: for every (word, bits) of R_r: v = U(snapshot); D_r = {v < phi - tol};
+//      write P_next (E/ifim.py:199-208).
+//   B: R_{r+1} = D_r | (N(D_r) & ~fixed), one thread per word over the whole
+//      bitmap (E/ifim.py:209-214, set form: membership only dedups), compacted
+//      into the next (word, bits) list.
+// ---------------------------------------------------------------------------
+
+constexpr int REM_U = 2;  // words in flight per warp in phase A
+
+template <int DIM, int SOL>
+__device__ __forceinline__ void rem_phase_a(const KP &p, const uint2 *__restrict__ Ec, unsigned n,
+                                            const double *__restrict__ Pc, double *__restrict__ Pn, uint32_t *Dc,
+                                            unsigned long long &a_dec, uint32_t gw, uint32_t GW)
+{
+    const unsigned lane = lane_id();
+    for (uint32_t base = gw * REM_U; base < n; base += GW * REM_U) {
+        uint2 e[REM_U];
+        WPos q[REM_U];
+        Sten s[REM_U];
+#pragma unroll
+        for (int u = 0; u < REM_U; ++u) {
+            const uint32_t i = base + u;
+            e[u] = (i < n) ? __ldcg(Ec + i) : make_uint2(0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < REM_U; ++u) {
+            q[u] = wpos<DIM>(p, e[u].x);
+            gather<DIM>(p, Pc, q[u], e[u].y, s[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < REM_U; ++u) {
+            const bool act = (e[u].y >> lane) & 1u;
+            const int64_t c = q[u].c0 + lane;
+            bool dec = false;
+            if (act) {
+                const double v = solve<DIM, SOL>(p, s[u], c);
+                dec = v < s[u].c - p.tol;  // E/ifim.py:203
+                Pn[c] = dec ? v : s[u].c;
+            }
+            const uint32_t dm = __ballot_sync(FULL, dec);
+            if (lane == 0 && e[u].y) {
+                Dc[e[u].x] = dm;
+                a_dec += __popc(dm);
+            }
+        }
+    }
+}
+
+template <int DIM>
+__device__ __forceinline__ void rem_phase_b(const KP &p, const uint32_t *__restrict__ Dc, uint32_t *Dn, uint2 *En,
+                                            unsigned *lenN, unsigned long long &a_next, unsigned *sscan)
+{
+    // chunks of BLOCK*4 words per block, thread t takes words base + t + k*BLOCK
+    constexpr int PER = 4;
+    const uint32_t chunk = BLOCK * PER;
+    const uint32_t planeW = (uint32_t)p.ny * p.W;
+    for (uint32_t base = blockIdx.x * chunk; base < p.nwords; base += gridDim.x * chunk) {
+        uint32_t wv[PER], rv[PER];
+        int cntf = 0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const uint32_t w = base + threadIdx.x + k * BLOCK;
+            wv[k] = w;
+            rv[k] = 0;
+            if (w < p.nwords) {
+                const uint32_t row = w / p.W;
+                const uint32_t wx = w - row * p.W;
+                uint32_t y, z;
+                if (DIM == 3) {
+                    z = row / (uint32_t)p.ny;
+                    y = row - z * (uint32_t)p.ny;
+                } else {
+                    z = 0;
+                    y = row;
+                }
+                const uint32_t c = ldcg(Dc + w);
+                uint32_t dil = (c << 1) | (c >> 1);
+                if (wx > 0) dil |= ldcg(Dc + w - 1) >> 31;
+                if (wx + 1 < p.W) dil |= ldcg(Dc + w + 1) << 31;
+                if (y > 0) dil |= ldcg(Dc + w - p.W);
+                if (y + 1 < p.ny) dil |= ldcg(Dc + w + p.W);
+                if (DIM == 3) {
+                    if (z > 0) dil |= ldcg(Dc + w - planeW);
+                    if (z + 1 < p.nz) dil |= ldcg(Dc + w + planeW);
+                }
+                const int64_t nv = p.nx - (int64_t)wx * 32;
+                const uint32_t rowm = nv >= 32 ? FULL : ((1u << nv) - 1u);
+                rv[k] = (c | (dil & ~__ldg(p.Bf + w))) & rowm;
+                Dn[w] = 0;  // D_{r+1} is written sparsely by the next phase A
+                if (rv[k]) {
+                    ++cntf;
+                    a_next += __popc(rv[k]);
+                }
+            }
+        }
+        // block exclusive scan of cntf
+        unsigned v = cntf;
+        const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned t = __shfl_up_sync(FULL, v, o);
+            if (lane >= (unsigned)o) v += t;
+        }
+        if (lane == 31) sscan[warp] = v;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned acc = 0;
+            for (int i = 0; i < WPB; ++i) {
+                const unsigned t = sscan[i];
+                sscan[i] = acc;
+                acc += t;
+            }
+            sscan[WPB] = acc ? atomicAdd(lenN, acc) : 0u;
+        }
+        __syncthreads();
+        unsigned pos = sscan[WPB] + sscan[warp] + v - cntf;
+#pragma unroll
+        for (int k = 0; k < PER; ++k)
+            if (rv[k]) En[pos++] = make_uint2(wv[k], rv[k]);
+        __syncthreads();
+    }
+}
+
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK) k_remedy(KP p, const unsigned *skip)
+{
+    __shared__ unsigned long long sred[WPB];
+    __shared__ unsigned sscan[WPB + 1];
+    if (skip && *skip) return;
+    const unsigned warp = threadIdx.x >> 5;
+    const uint32_t gw = blockIdx.x * WPB + warp;
+    const uint32_t GW = gridDim.x * WPB;
+    Ctl *ctl = p.ctl;
+    unsigned long long a_dec = 0;
+    const unsigned long long r0 = vload(&ctl->cnt[0]);
+    if (r0 == 0) return;  // empty remedy set: zero rounds
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->peak = r0;
+        ctl->sum = 0;
+    }
+    const uint2 *E[2] = {reinterpret_cast<const uint2 *>(p.L0), reinterpret_cast<const uint2 *>(p.L1)};
+    for (int64_t r = 0;; ++r) {
+        const int par = (int)(r & 1);
+        const double *Pc = par ? p.P1 : p.P0;
+        double *Pn = par ? p.P0 : p.P1;
+        uint32_t *Dc = par ? p.B1 : p.B0;
+        uint32_t *Dn = par ? p.B0 : p.B1;
+        const unsigned n = vload(&ctl->len[r % 3]);
+        rem_phase_a<DIM, SOL>(p, E[par], n, Pc, Pn, Dc, a_dec, gw, GW);
+        grid_barrier(ctl);
+        unsigned long long a_next = 0;
+        rem_phase_b<DIM>(p, Dc, Dn, const_cast<uint2 *>(E[par ^ 1]), &ctl->len[(r + 1) % 3], a_next, sscan);
+        const unsigned long long tot = block_sum(a_next, sred);
+        if (threadIdx.x == 0) {
+            if (tot) atomicAdd(&ctl->cnt[(r + 1) % 3], tot);
+            if (blockIdx.x == 0) {
+                ctl->len[(r + 2) % 3] = 0;
+                ctl->cnt[(r + 2) % 3] = 0;
+            }
+        }
+        grid_barrier(ctl);
+        const unsigned long long m = vload(&ctl->cnt[(r + 1) % 3]);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctl->iters = r + 1;
+            ctl->sum += vload(&ctl->cnt[r % 3]);
+            if (m > ctl->peak) ctl->peak = m;
+        }
+        if (m == 0) break;
+        if (r + 1 >= p.cap) {  // E/ifim.py:185-189
+            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
+            break;
+        }
+    }
+    const unsigned long long td = block_sum(a_dec, sred);
+    if (threadIdx.x == 0) atomicAdd(&ctl->writes, td);
+}
+
+// Element-wise local solver (parity hook).
+__global__ void k_local(int kind, const double *a, const double *b, const double *c, const double *f, double dx,
+                        double dy, double *out, int64_t n)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (kind == 0) out[i] = upd2u(a[i], b[i], dx / f[i]);
+        else if (kind == 1) out[i] = upd2a(a[i], b[i], f[i], dx, dy);
+        else out[i] = upd3u(a[i], b[i], c[i], dx / f[i], dx);
+    }
+}
+
+// Copy P1 into P0 (used only on the error path to expose the latest field).
+__global__ void k_copy(double *dst, const double *src, int64_t n)
+{
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(call)                                                                              \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess) return fail(EIK_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+    } while (0)
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+struct Layout {
+    int64_t N;
+    uint32_t W, nwords;
+    size_t off_phi2, off_dd, off_b0, off_b1, off_bt, off_bf, off_l0, off_l1, off_hist, off_ctl_u, off_ctl_r, total;
+    int64_t cap_upd, cap_rem;
+};
+
+int make_layout(const eik_geom *g, Layout &L)
+{
+    if (!g) return fail(EIK_EINVAL, "null geometry");
+    if (g->ndim != 2 && g->ndim != 3) return fail(EIK_EINVAL, "ndim must be 2 or 3, got %d", g->ndim);
+    if (g->nx < 1 || g->ny < 1 || g->nz < 1) return fail(EIK_EINVAL, "grid must have at least one cell");
+    if (g->ndim == 2 && g->nz != 1) return fail(EIK_EINVAL, "2D grid must have nz == 1");
+    if (!(g->dx > 0) || !(g->dy > 0) || !(g->dz > 0)) return fail(EIK_EINVAL, "grid spacing must be positive");
+    if (g->ndim == 3 && !(g->dx == g->dy && g->dy == g->dz))
+        return fail(EIK_EINVAL, "3D grids require dx == dy == dz (no anisotropic 3D solver, SPEC.md:169)");
+    if (g->dtype != EIK_F64) return fail(EIK_EINVAL, "only float64 is supported");
+    L.N = g->nx * g->ny * g->nz;
+    const int64_t W = (g->nx + 31) / 32;
+    const int64_t nw = W * g->ny * g->nz;
+    if (nw >= (int64_t)1 << 31 || L.N >= (int64_t)1 << 40) return fail(EIK_EINVAL, "grid too large");
+    L.W = (uint32_t)W;
+    L.nwords = (uint32_t)nw;
+    const int64_t s = g->nx + g->ny + (g->ndim == 3 ? g->nz : 0);
+    L.cap_upd = 40 * s;  // E/ifim.py:106 (2D: 40*(nx+ny))
+    L.cap_rem = 20 * s;  // E/ifim.py:185
+    size_t o = 0;
+    L.off_phi2 = o; o += al((size_t)L.N * 8);
+    L.off_dd = o; o += al((size_t)L.N * 8);
+    L.off_b0 = o; o += al((size_t)nw * 4);
+    L.off_b1 = o; o += al((size_t)nw * 4);
+    L.off_bt = o; o += al((size_t)nw * 4);
+    L.off_bf = o; o += al((size_t)nw * 4);
+    L.off_l0 = o; o += al((size_t)nw * 8);
+    L.off_l1 = o; o += al((size_t)nw * 8);
+    L.off_hist = o; o += al((size_t)(L.cap_upd + 2) * 8);
+    L.off_ctl_u = o; o += al(sizeof(Ctl));
+    L.off_ctl_r = o; o += al(sizeof(Ctl));
+    L.total = o;
+    return EIK_OK;
+}
+
+int solver_kind(const eik_geom *g)
+{
+    if (g->ndim == 3) return SOL_U3;
+    return g->dx == g->dy ? SOL_U2 : SOL_A2;  // E/_kernels.py:41-44
+}
+
+KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const double *speed, const uint8_t *state,
+           double tol, Ctl *ctl, int64_t cap)
+{
+    char *b = (char *)ws;
+    KP p;
+    memset(&p, 0, sizeof(p));
+    p.nx = g->nx; p.ny = g->ny; p.nz = g->nz; p.plane = g->nx * g->ny;
+    p.W = L.W; p.nwords = L.nwords; p.nrows = (uint32_t)(g->ny * g->nz);
+    p.dx = g->dx; p.dy = g->dy; p.delta = g->dx; p.tol = tol;
+    p.P0 = phi;
+    p.P1 = (double *)(b + L.off_phi2);
+    p.F = speed;
+    p.dd = (double *)(b + L.off_dd);
+    p.state = state;
+    p.B0 = (uint32_t *)(b + L.off_b0);
+    p.B1 = (uint32_t *)(b + L.off_b1);
+    p.Bt = (uint32_t *)(b + L.off_bt);
+    p.Bf = (uint32_t *)(b + L.off_bf);
+    p.L0 = (uint32_t *)(b + L.off_l0);
+    p.L1 = (uint32_t *)(b + L.off_l1);
+    p.ctl = ctl;
+    p.hist = (int64_t *)(b + L.off_hist);
+    p.hist_cap = L.cap_upd + 2;
+    p.cap = cap;
+    return p;
+}
+
+int g_sms = 0;
+
+int num_sms()
+{
+    if (!g_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_sms <= 0) g_sms = 148;
+    }
+    return g_sms;
+}
+
+int stream_grid(int64_t work_warps)
+{
+    int64_t blocks = (work_warps + WPB - 1) / WPB;
+    const int64_t mx = (int64_t)num_sms() * 8;
+    if (blocks > mx) blocks = mx;
+    if (blocks < 1) blocks = 1;
+    return (int)blocks;
+}
+
+template <typename K>
+int coop_launch(K kernel, KP &p, const unsigned *skip, bool with_skip, cudaStream_t st)
+{
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, BLOCK, 0);
+    if (e != cudaSuccess) return fail(EIK_ECUDA, "occupancy: %s", cudaGetErrorString(e));
+    if (const char *env = getenv("EIK_BLOCKS_PER_SM")) {
+        const int v = atoi(env);
+        if (v > 0 && v < per_sm) per_sm = v;
+    }
+    if (per_sm < 1) return fail(EIK_ECUDA, "persistent kernel cannot be resident");
+    dim3 grid(per_sm * num_sms()), block(BLOCK);
+    void *args2[] = {&p, (void *)&skip};
+    void *args1[] = {&p};
+    e = cudaLaunchCooperativeKernel((const void *)kernel, grid, block, with_skip ? args2 : args1, 0, st);
+    if (e != cudaSuccess) return fail(EIK_ECUDA, "cooperative launch: %s", cudaGetErrorString(e));
+    return EIK_OK;
+}
+
+template <int DIM, int SOL>
+struct Engine {
+    static int prep(KP &p, bool copy_phi, bool touched, uint32_t *c0, uint32_t *c1, cudaStream_t st)
+    {
+        const int grid = stream_grid(p.nwords);
+        if (SOL == SOL_A2) k_prep<false><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched, c0, c1);
+        else k_prep<true><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched, c0, c1);
+        CK(cudaGetLastError());
+        return EIK_OK;
+    }
+    static int init_active(KP &p, const int64_t *seeds, int64_t ns, cudaStream_t st)
+    {
+        const int grid = (int)std::min<int64_t>((ns + 255) / 256, 1024);
+        k_init_active<DIM><<<grid > 0 ? grid : 1, 256, 0, st>>>(p, seeds, ns);
+        CK(cudaGetLastError());
+        return EIK_OK;
+    }
+    static int update(KP &p, cudaStream_t st) { return coop_launch(k_update<DIM, SOL>, p, nullptr, false, st); }
+    static int build(KP &p, const double *Pc, const unsigned *skip, cudaStream_t st)
+    {
+        const int grid = stream_grid(p.nwords);
+        k_build<DIM, SOL><<<grid, BLOCK, 0, st>>>(p, Pc, reinterpret_cast<uint2 *>(p.L0), p.B0, skip);
+        CK(cudaGetLastError());
+        return EIK_OK;
+    }
+    static int remedy(KP &p, const unsigned *skip, cudaStream_t st)
+    {
+        return coop_launch(k_remedy<DIM, SOL>, p, skip, true, st);
+    }
+};
+
+template <typename F>
+int dispatch(const eik_geom *g, F &&f)
+{
+    switch (solver_kind(g)) {
+        case SOL_U2: return f(Engine<2, SOL_U2>());
+        case SOL_A2: return f(Engine<2, SOL_A2>());
+        default: return f(Engine<3, SOL_U3>());
+    }
+}
+
+struct Events {
+    cudaEvent_t e[8];
+    int n = 0;
+    Events() { for (auto &x : e) cudaEventCreate(&x); }
+    ~Events() { for (auto &x : e) cudaEventDestroy(x); }
+    void rec(int i, cudaStream_t s) { cudaEventRecord(e[i], s); }
+    float ms(int a, int b)
+    {
+        float t = 0;
+        cudaEventElapsedTime(&t, e[a], e[b]);
+        return t;
+    }
+};
+
+int check_ws(const Layout &L, void *ws, size_t bytes)
+{
+    if (!ws) return fail(EIK_EINVAL, "null workspace");
+    if (bytes < L.total) return fail(EIK_EINVAL, "workspace too small: %zu < %zu", bytes, L.total);
+    if ((uintptr_t)ws & 255) return fail(EIK_EINVAL, "workspace must be 256-byte aligned");
+    return EIK_OK;
+}
+
+// Phases shared by solve and the staged entry points --------------------------------
+
+int run_update(const eik_geom *g, const Layout &L, double *phi, const double *speed, uint8_t *state,
+               const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol, void *ws,
+               cudaStream_t st, int64_t &launches)
+{
+    char *b = (char *)ws;
+    Ctl *ctl = (Ctl *)(b + L.off_ctl_u);
+    CK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
+    if (nseeds > 0) {
+        k_seed<<<(int)std::min<int64_t>((nseeds + 255) / 256, 1024), 256, 0, st>>>(phi, state, seed_idx, seed_val,
+                                                                                   nseeds);
+        CK(cudaGetLastError());
+        ++launches;
+    }
+    KP p = make_kp(g, L, ws, phi, speed, state, tol, ctl, L.cap_upd);
+    return dispatch(g, [&](auto E) {
+        int rc = E.prep(p, true, true, p.B0, p.B1, st);
+        if (rc) return rc;
+        rc = E.init_active(p, seed_idx, nseeds, st);
+        if (rc) return rc;
+        rc = E.update(p, st);
+        launches += 3;
+        return rc;
+    });
+}
+
+void fill_update_stats(const Ctl &c, eik_stats *o)
+{
+    o->upd_iterations = (int64_t)c.iters;
+    o->upd_calls = (int64_t)c.sum;
+    o->peak_active = (int64_t)c.peak;
+    o->converged = (int64_t)c.conv;
+    o->history_len = (int64_t)c.iters;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+
+extern "C" {
+
+const char *eik_last_error(void) { return g_err.c_str(); }
+
+const char *eik_version(void) { return "eik_ifim 0.1 (sm_100a, float64 bit-exact, persistent grid-barrier engine)"; }
+
+int eik_workspace_size(const eik_geom *g, size_t *bytes)
+{
+    Layout L;
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if (!bytes) return fail(EIK_EINVAL, "null output");
+    *bytes = L.total;
+    return EIK_OK;
+}
+
+int eik_ifim_update_step(const eik_geom *g, double *phi, const double *speed, uint8_t *state,
+                         const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
+                         void *workspace, size_t workspace_bytes, int64_t *history, int64_t history_cap,
+                         eik_stats *out, void *stream)
+{
+    Layout L;
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if ((rc = check_ws(L, workspace, workspace_bytes))) return rc;
+    if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
+    if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
+    if (nseeds < 1 || !seed_idx || !seed_val) return fail(EIK_EINVAL, "boundary condition has no seeds");
+    cudaStream_t st = (cudaStream_t)stream;
+    memset(out, 0, sizeof(*out));
+    Events ev;
+    ev.rec(0, st);
+    int64_t launches = 0;
+    rc = run_update(g, L, phi, speed, state, seed_idx, seed_val, nseeds, tol, workspace, st, launches);
+    if (rc) return rc;
+    ev.rec(1, st);
+    Ctl c;
+    char *b = (char *)workspace;
+    CK(cudaMemcpyAsync(&c, b + L.off_ctl_u, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (c.err == EIK_ECAP && (c.iters & 1)) {  // expose the latest buffer like the reference would
+        k_copy<<<1024, 256, 0, st>>>(phi, (const double *)(b + L.off_phi2), L.N);
+        CK(cudaStreamSynchronize(st));
+    }
+    fill_update_stats(c, out);
+    out->iterations = out->upd_iterations;
+    out->solver_calls = out->upd_calls;
+    out->phi_writes = (int64_t)c.writes;
+    out->gpu_launches = launches;
+    out->upd_ms = out->total_ms = ev.ms(0, 1);
+    if (history && history_cap > 0 && c.iters > 0) {
+        const int64_t n = std::min<int64_t>((int64_t)c.iters, history_cap);
+        CK(cudaMemcpy(history, b + L.off_hist, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    }
+    if (c.err == EIK_ECAP)
+        return fail(EIK_ECAP, "active list did not drain within %lld iterations", (long long)L.cap_upd);
+    return EIK_OK;
+}
+
+int eik_build_remedy(const eik_geom *g, const double *phi, const double *speed, const uint8_t *state, double tol,
+                     void *workspace, size_t workspace_bytes, eik_stats *out, void *stream)
+{
+    Layout L;
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if ((rc = check_ws(L, workspace, workspace_bytes))) return rc;
+    if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
+    if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
+    cudaStream_t st = (cudaStream_t)stream;
+    memset(out, 0, sizeof(*out));
+    char *b = (char *)workspace;
+    Ctl *ctl = (Ctl *)(b + L.off_ctl_r);
+    Events ev;
+    ev.rec(0, st);
+    CK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
+    KP p = make_kp(g, L, workspace, const_cast<double *>(phi), speed, state, tol, ctl, L.cap_rem);
+    rc = dispatch(g, [&](auto E) {
+        int r = E.prep(p, false, false, nullptr, nullptr, st);
+        if (r) return r;
+        return E.build(p, phi, nullptr, st);
+    });
+    if (rc) return rc;
+    ev.rec(1, st);
+    Ctl c;
+    CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    out->build_calls = out->solver_calls = (int64_t)c.free_cells;
+    out->remedy_size = (int64_t)c.flagged;
+    out->gpu_launches = 2;
+    out->build_ms = out->total_ms = ev.ms(0, 1);
+    return EIK_OK;
+}
+
+int eik_remedy_load(const eik_geom *g, const uint8_t *member, const uint8_t *state, void *workspace,
+                    size_t workspace_bytes, int64_t *count, void *stream)
+{
+    Layout L;
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if ((rc = check_ws(L, workspace, workspace_bytes))) return rc;
+    if (!member) return fail(EIK_EINVAL, "null member mask");
+    cudaStream_t st = (cudaStream_t)stream;
+    char *b = (char *)workspace;
+    Ctl *ctl = (Ctl *)(b + L.off_ctl_r);
+    CK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
+    KP p = make_kp(g, L, workspace, nullptr, nullptr, state, 1e-12, ctl, L.cap_rem);
+    k_remedy_load<<<stream_grid(p.nwords), BLOCK, 0, st>>>(p, member, reinterpret_cast<uint2 *>(p.L0), p.B0);
+    CK(cudaGetLastError());
+    Ctl c;
+    CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (count) *count = (int64_t)c.cnt[0];
+    return EIK_OK;
+}
+
+int eik_remedy_export(const eik_geom *g, void *workspace, size_t workspace_bytes, uint8_t *member, void *stream)
+{
+    Layout L;
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if ((rc = check_ws(L, workspace, workspace_bytes))) return rc;
+    if (!member) return fail(EIK_EINVAL, "null member mask");
+    cudaStream_t st = (cudaStream_t)stream;
+    char *b = (char *)workspace;
+    Ctl c;
+    CK(cudaMemcpyAsync(&c, b + L.off_ctl_r, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaMemsetAsync(member, 0, (size_t)L.N, st));
+    KP p = make_kp(g, L, workspace, nullptr, nullptr, nullptr, 1e-12, nullptr, 0);
+    if (c.len[0]) {
+        k_remedy_export<<<stream_grid(c.len[0]), BLOCK, 0, st>>>(p, reinterpret_cast<const uint2 *>(p.L0), c.len[0],
+                                                                 member);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(st));
+    return EIK_OK;
+}
+
+int eik_remedy_step(const eik_geom *g, double *phi, const double *speed, const uint8_t *state, double tol,
+                    void *workspace, size_t workspace_bytes, eik_stats *out, void *stream)
+{
+    Layout L;
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if ((rc = check_ws(L, workspace, workspace_bytes))) return rc;
+    if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
+    if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
+    cudaStream_t st = (cudaStream_t)stream;
+    memset(out, 0, sizeof(*out));
+    char *b = (char *)workspace;
+    Ctl *ctl = (Ctl *)(b + L.off_ctl_r);
+    Events ev;
+    ev.rec(0, st);
+    KP p = make_kp(g, L, workspace, phi, speed, state, tol, ctl, L.cap_rem);
+    // staged call: the caller may have edited phi since the last call
+    rc = dispatch(g, [&](auto E) {
+        int r = E.prep(p, true, false, nullptr, nullptr, st);
+        if (r) return r;
+        return E.remedy(p, nullptr, st);
+    });
+    if (rc) return rc;
+    ev.rec(1, st);
+    Ctl c;
+    CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (c.err == EIK_ECAP && (c.iters & 1)) {
+        k_copy<<<1024, 256, 0, st>>>(phi, p.P1, L.N);
+        CK(cudaStreamSynchronize(st));
+    }
+    out->rem_iterations = out->iterations = (int64_t)c.iters;
+    out->rem_calls = out->solver_calls = (int64_t)c.sum;
+    out->peak_remedy = (int64_t)c.peak;
+    out->phi_writes = (int64_t)c.writes;
+    out->gpu_launches = 2;
+    out->rem_ms = out->total_ms = ev.ms(0, 1);
+    if (c.err == EIK_ECAP) return fail(EIK_ECAP, "remedy set did not drain within %lld rounds", (long long)L.cap_rem);
+    return EIK_OK;
+}
+
+int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t *state, const int64_t *seed_idx,
+                   const double *seed_val, int64_t nseeds, double tol, void *workspace, size_t workspace_bytes,
+                   int64_t *history, int64_t history_cap, eik_stats *out, void *stream)
+{
+    Layout L;
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if ((rc = check_ws(L, workspace, workspace_bytes))) return rc;
+    if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
+    if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
+    if (nseeds < 1 || !seed_idx || !seed_val) return fail(EIK_EINVAL, "boundary condition has no seeds");
+    cudaStream_t st = (cudaStream_t)stream;
+    memset(out, 0, sizeof(*out));
+    char *b = (char *)workspace;
+    Ctl *cu = (Ctl *)(b + L.off_ctl_u);
+    Ctl *cr = (Ctl *)(b + L.off_ctl_r);
+    Events ev;
+    int64_t launches = 0;
+    ev.rec(0, st);
+    rc = run_update(g, L, phi, speed, state, seed_idx, seed_val, nseeds, tol, workspace, st, launches);
+    if (rc) return rc;
+    ev.rec(1, st);
+    CK(cudaMemsetAsync(cr, 0, sizeof(Ctl), st));
+    KP p = make_kp(g, L, workspace, phi, speed, state, tol, cr, L.cap_rem);
+    // After a drained update step both phi buffers are identical (every cell
+    // changed in the last-but-one iteration rewrote itself in the last one),
+    // so the build reads the caller's buffer and the remedy starts at parity 0.
+    const unsigned *skip = &cu->err;
+    rc = dispatch(g, [&](auto E) { return E.build(p, phi, skip, st); });
+    if (rc) return rc;
+    ev.rec(2, st);
+    rc = dispatch(g, [&](auto E) { return E.remedy(p, skip, st); });
+    if (rc) return rc;
+    ev.rec(3, st);
+    launches += 2;
+    Ctl c[2];
+    CK(cudaMemcpyAsync(&c[0], cu, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&c[1], cr, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (c[0].err == EIK_ECAP) {
+        if (c[0].iters & 1) {
+            k_copy<<<1024, 256, 0, st>>>(phi, p.P1, L.N);
+            CK(cudaStreamSynchronize(st));
+        }
+        return fail(EIK_ECAP, "active list did not drain within %lld iterations", (long long)L.cap_upd);
+    }
+    if (c[1].err == EIK_ECAP) {
+        if (c[1].iters & 1) {
+            k_copy<<<1024, 256, 0, st>>>(phi, p.P1, L.N);
+            CK(cudaStreamSynchronize(st));
+        }
+        return fail(EIK_ECAP, "remedy set did not drain within %lld rounds", (long long)L.cap_rem);
+    }
+    fill_update_stats(c[0], out);
+    out->build_calls = (int64_t)c[1].free_cells;
+    out->remedy_size = (int64_t)c[1].flagged;
+    out->rem_iterations = (int64_t)c[1].iters;
+    out->rem_calls = (int64_t)c[1].sum;
+    out->peak_remedy = (int64_t)c[1].peak;
+    out->iterations = out->upd_iterations + out->rem_iterations;  // E/ifim.py:227-233
+    out->solver_calls = out->upd_calls + out->build_calls + out->rem_calls;
+    out->phi_writes = (int64_t)(c[0].writes + c[1].writes);
+    out->gpu_launches = launches;
+    out->upd_ms = ev.ms(0, 1);
+    out->build_ms = ev.ms(1, 2);
+    out->rem_ms = ev.ms(2, 3);
+    out->total_ms = ev.ms(0, 3);
+    if (history && history_cap > 0 && c[0].iters > 0) {
+        const int64_t n = std::min<int64_t>((int64_t)c[0].iters, history_cap);
+        CK(cudaMemcpy(history, b + L.off_hist, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    }
+    return EIK_OK;
+}
+
+int eik_local_solve(int kind, const double *a, const double *b, const double *c, const double *f, double dx,
+                    double dy, double *out, int64_t n, void *stream)
+{
+    if (kind < 0 || kind > 2) return fail(EIK_EINVAL, "kind must be 0, 1 or 2");
+    if (!a || !b || !f || !out || (kind == 2 && !c)) return fail(EIK_EINVAL, "null array");
+    if (n <= 0) return EIK_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_local<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(kind, a, b, c, f, dx, dy, out, n);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return EIK_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,385 @@
+"""Drop-in iFIM entry points backed by the B200 engine.
+
+Same names, signatures, argument meaning, return types and error behaviour as
+the reference's E/ifim.py (E = /root/reference/pkg/src/eikonal):
+
+    solve_ifim(grid, bc, tol=1e-12, workers=1) -> SolverResult     E/ifim.py:221-235
+    ifim_update_step(grid, bc, tol=1e-12, workers=1) -> RunStats   E/ifim.py:75-134
+    build_remedy_set(grid, tol=1e-12, workers=1) -> (RemedySet, int)  E/ifim.py:137-161
+    ifim_remedy_step(grid, remedy, tol=1e-12, workers=1) -> RunStats  E/ifim.py:164-218
+    RemedySet                                                      E/ifim.py:64-72
+
+The solvers mutate ``grid.phi`` in place, mark seeds SOURCE in ``grid.state``
+and start from whatever phi they are given.  ``workers`` is validated like
+E/parallel.py:28-42 and otherwise ignored: the work runs on the GPU through
+the C ABI in include/eik_ifim.h.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import time
+
+import numpy as np
+import torch
+
+from . import _native
+from .grid import CellState, seed_linear
+from .result import RunStats, SolverResult
+
+
+def resolve_workers(workers: int | None = None) -> int:
+    """E/parallel.py:28-42 (validation only; the device engine ignores the count)."""
+    if workers is None:
+        env = os.environ.get("EIKONAL_WORKERS", "").strip()
+        workers = int(env) if env else 1
+    workers = int(workers)
+    if workers == 0:
+        return os.cpu_count() or 1
+    if workers < 0:
+        raise ValueError(f"worker count must be >= 0, got {workers}")
+    return workers
+
+
+def _check_tol(tol: float) -> None:
+    if tol <= 0:
+        raise ValueError(f"tol must be positive, got {tol}")
+
+
+# ---------------------------------------------------------------------------
+# device views of a grid
+# ---------------------------------------------------------------------------
+
+def _is_cuda_tensor(x) -> bool:
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _pick_device(grid) -> torch.device:
+    if _is_cuda_tensor(grid.phi):
+        return grid.phi.device
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2106_15869_b200 needs a CUDA device (B200); no CPU fallback exists")
+    dev = os.environ.get("EIKONAL_DEVICE", "cuda:0")
+    return torch.device(dev)
+
+
+def geometry(grid) -> _native.Geom:
+    if getattr(grid, "ndim", 2) == 3:
+        h = float(grid.h)
+        return _native.Geom(int(grid.nx), int(grid.ny), int(grid.nz), h, h, h, 3, 0)
+    return _native.Geom(int(grid.nx), int(grid.ny), 1, float(grid.dx), float(grid.dy), float(grid.dx), 2, 0)
+
+
+class _DeviceGrid:
+    """phi / speed / state of a grid as contiguous CUDA tensors.
+
+    CUDA-tensor grids are used in place.  Host grids (numpy arrays or CPU
+    tensors) are uploaded and ``commit`` writes phi (and state) back into the
+    caller's arrays, which is what the in-place reference API promises.
+    """
+
+    def __init__(self, grid, need_phi=True, need_state=True):
+        self.grid = grid
+        self.device = _pick_device(grid)
+        self.host = not _is_cuda_tensor(grid.phi)
+        self.phi = self._dev(grid.phi, torch.float64) if need_phi else None
+        self.speed = self._dev(grid.speed, torch.float64)
+        self.state = self._dev(grid.state, torch.uint8) if need_state else None
+
+    def _dev(self, arr, dtype):
+        if _is_cuda_tensor(arr):
+            if arr.dtype != dtype or not arr.is_contiguous():
+                raise ValueError(f"CUDA grid arrays must be contiguous {dtype}, got {arr.dtype}")
+            if arr.device != self.device:
+                raise ValueError("grid arrays live on different devices")
+            return arr
+        t = torch.as_tensor(np.ascontiguousarray(arr)) if isinstance(arr, np.ndarray) else arr
+        return t.to(device=self.device, dtype=dtype).contiguous()
+
+    @property
+    def stream(self):
+        return C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def commit(self, phi=True, state=False):
+        if not self.host:
+            return
+        torch.cuda.synchronize(self.device)
+        if phi:
+            _copy_into(self.grid.phi, self.phi)
+        if state:
+            _copy_into(self.grid.state, self.state)
+
+
+def _copy_into(host_arr, dev_t):
+    if isinstance(host_arr, np.ndarray):
+        torch.from_numpy(host_arr).copy_(dev_t.reshape(host_arr.shape))
+    else:
+        host_arr.copy_(dev_t.reshape(host_arr.shape))
+
+
+def _host_mark_sources(grid, idx):
+    """apply_boundary's state write (E/grid.py:215) on a host grid."""
+    st = grid.state
+    flat = st.reshape(-1)
+    for c in idx:
+        flat[c] = CellState.SOURCE
+
+
+# ---------------------------------------------------------------------------
+# workspace cache (the caller owns all device memory; the library allocates none)
+# ---------------------------------------------------------------------------
+
+class Workspace:
+    def __init__(self, geom: _native.Geom, device: torch.device):
+        n = C.c_size_t(0)
+        _native.check(_native.lib().eik_workspace_size(C.byref(geom), C.byref(n)))
+        self.nbytes = int(n.value)
+        self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+        self.gen = 0  # bumped by every call that rewrites the remedy set slots
+
+    @property
+    def ptr(self):
+        return C.c_void_p(self.buf.data_ptr())
+
+
+_WS: dict = {}
+
+
+def workspace(geom: _native.Geom, device: torch.device) -> Workspace:
+    key = (str(device), geom.nx, geom.ny, geom.nz, geom.ndim)
+    ws = _WS.get(key)
+    if ws is None:
+        if len(_WS) >= 4:
+            _WS.clear()
+        ws = Workspace(geom, device)
+        _WS[key] = ws
+    return ws
+
+
+def clear_workspaces() -> None:
+    _WS.clear()
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+def _history_cap(g: _native.Geom) -> int:
+    return 40 * (g.nx + g.ny + (g.nz if g.ndim == 3 else 0)) + 2
+
+
+# ---------------------------------------------------------------------------
+# RemedySet
+# ---------------------------------------------------------------------------
+
+class RemedySet:
+    """Cells flagged for repair (E/ifim.py:64-72): ``member`` mask + ``cells`` list.
+
+    Sets produced by build_remedy_set live on the device; ``member`` and
+    ``cells`` are materialised on first access.  A RemedySet built by hand from
+    a member mask (and/or a cell list) is accepted by ifim_remedy_step too.
+    """
+
+    def __init__(self, member=None, cells=None, *, _device=None):
+        self._member = member
+        self._cells = [int(c) for c in cells] if cells is not None else None
+        self._dev = _device  # dict(mask, count, ws, gen, host, shape)
+
+    def __len__(self) -> int:
+        if self._dev is not None:
+            return int(self._dev["count"])
+        if self._cells is not None:
+            return len(self._cells)
+        m = self._member
+        return int(m.sum()) if m is not None else 0
+
+    @property
+    def member(self):
+        if self._member is None and self._dev is not None:
+            mask = self._dev["mask"].bool()  # flat (N,), like E/ifim.py:158
+            self._member = mask.cpu().numpy() if self._dev["host"] else mask
+        return self._member
+
+    @member.setter
+    def member(self, value):
+        self._member = value
+        self._dev = None
+
+    @property
+    def cells(self) -> list:
+        if self._cells is None:
+            m = self.member
+            if m is None:
+                self._cells = []
+            elif isinstance(m, torch.Tensor):
+                self._cells = torch.nonzero(m.reshape(-1)).reshape(-1).cpu().tolist()
+            else:
+                self._cells = np.flatnonzero(np.asarray(m).reshape(-1)).tolist()
+        return self._cells
+
+    @cells.setter
+    def cells(self, value):
+        self._cells = [int(c) for c in value]
+        self._member = None
+        self._dev = None
+
+    def _drain(self):
+        """After ifim_remedy_step the set is empty (E/ifim.py:186, :208)."""
+        if self._dev is not None:
+            self._dev["count"] = 0
+            self._dev["mask"].zero_()
+        if self._member is not None:
+            if isinstance(self._member, torch.Tensor):
+                self._member.zero_()
+            else:
+                self._member[...] = False
+        self._cells = []
+
+    def _device_mask(self, shape, device) -> torch.Tensor:
+        if self._dev is not None:
+            return self._dev["mask"]
+        n = int(np.prod(shape))
+        if self._member is not None:
+            m = self._member
+            t = m if isinstance(m, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(m))
+            return t.reshape(-1).to(device=device, dtype=torch.uint8).contiguous()
+        mask = torch.zeros(n, dtype=torch.uint8, device=device)
+        if self._cells:
+            mask[torch.as_tensor(self._cells, dtype=torch.int64, device=device)] = 1
+        return mask
+
+
+# ---------------------------------------------------------------------------
+# entry points
+# ---------------------------------------------------------------------------
+
+def _stats_from(s: _native.Stats) -> dict:
+    return s.as_dict()
+
+
+def ifim_update_step(grid, bc, tol: float = 1e-12, workers: int = 1) -> RunStats:
+    """Drain the active list without neighbour convergence checks (E/ifim.py:75-134)."""
+    _check_tol(tol)
+    resolve_workers(workers)
+    idx, val = seed_linear(grid, bc)
+    dg = _DeviceGrid(grid)
+    geom = geometry(grid)
+    ws = workspace(geom, dg.device)
+    ws.gen += 1
+    si = torch.as_tensor(idx, dtype=torch.int64, device=dg.device)
+    sv = torch.as_tensor(val, dtype=torch.float64, device=dg.device)
+    hcap = _history_cap(geom)
+    hist = np.zeros(hcap, dtype=np.int64)
+    st = _native.Stats()
+    rc = _native.lib().eik_ifim_update_step(
+        C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), _ptr(si), _ptr(sv), len(idx), float(tol),
+        ws.ptr, ws.nbytes, hist.ctypes.data_as(C.c_void_p), hcap, C.byref(st), dg.stream)
+    if dg.host:
+        _host_mark_sources(grid, idx)
+        dg.commit(phi=True)
+    _native.check(rc)
+    d = _stats_from(st)
+    stats = RunStats(active_history=hist[: d["upd_iterations"]].tolist())
+    stats.iterations = d["upd_iterations"]
+    stats.solver_calls = d["upd_calls"]
+    stats.peak_active = d["peak_active"]
+    stats.phi_writes = d["phi_writes"]
+    stats.phases = {"update": d}
+    stats.device_ms = {"update": d["upd_ms"]}
+    stats.gpu_launches = d["gpu_launches"]
+    return stats
+
+
+def build_remedy_set(grid, tol: float = 1e-12, workers: int = 1):
+    """One full verification pass; returns (RemedySet, solver calls) (E/ifim.py:137-161)."""
+    _check_tol(tol)
+    resolve_workers(workers)
+    dg = _DeviceGrid(grid)
+    geom = geometry(grid)
+    ws = workspace(geom, dg.device)
+    ws.gen += 1
+    st = _native.Stats()
+    _native.check(_native.lib().eik_build_remedy(
+        C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), float(tol), ws.ptr, ws.nbytes,
+        C.byref(st), dg.stream))
+    n = int(np.prod(tuple(int(s) for s in grid.phi.shape)))
+    mask = torch.empty(n, dtype=torch.uint8, device=dg.device)
+    _native.check(_native.lib().eik_remedy_export(C.byref(geom), ws.ptr, ws.nbytes, _ptr(mask), dg.stream))
+    remedy = RemedySet(_device={"mask": mask, "count": int(st.remedy_size), "ws": ws, "gen": ws.gen,
+                                "host": dg.host, "shape": tuple(grid.phi.shape)})
+    return remedy, int(st.build_calls)
+
+
+def ifim_remedy_step(grid, remedy: RemedySet, tol: float = 1e-12, workers: int = 1) -> RunStats:
+    """Relax the remedy set to quiescence, accepting only decreases (E/ifim.py:164-218)."""
+    _check_tol(tol)
+    resolve_workers(workers)
+    dg = _DeviceGrid(grid)
+    geom = geometry(grid)
+    ws = workspace(geom, dg.device)
+    fresh = (remedy._dev is not None and remedy._dev.get("ws") is ws and remedy._dev.get("gen") == ws.gen)
+    if not fresh:
+        mask = remedy._device_mask(tuple(grid.phi.shape), dg.device)
+        cnt = C.c_int64(0)
+        _native.check(_native.lib().eik_remedy_load(C.byref(geom), _ptr(mask), _ptr(dg.state), ws.ptr, ws.nbytes,
+                                                    C.byref(cnt), dg.stream))
+    ws.gen += 1
+    st = _native.Stats()
+    rc = _native.lib().eik_remedy_step(C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), float(tol),
+                                       ws.ptr, ws.nbytes, C.byref(st), dg.stream)
+    dg.commit(phi=True)
+    _native.check(rc)
+    remedy._drain()
+    d = _stats_from(st)
+    stats = RunStats()
+    stats.iterations = d["rem_iterations"]
+    stats.solver_calls = d["rem_calls"]
+    stats.peak_remedy = d["peak_remedy"]
+    stats.phi_writes = d["phi_writes"]
+    stats.phases = {"remedy": d}
+    stats.device_ms = {"remedy": d["rem_ms"]}
+    stats.gpu_launches = d["gpu_launches"]
+    return stats
+
+
+def solve_ifim(grid, bc, tol: float = 1e-12, workers: int = 1) -> SolverResult:
+    """Update step + build + remedy, device-resident (E/ifim.py:221-235)."""
+    t0 = time.perf_counter()
+    _check_tol(tol)
+    resolve_workers(workers)
+    idx, val = seed_linear(grid, bc)
+    dg = _DeviceGrid(grid)
+    geom = geometry(grid)
+    ws = workspace(geom, dg.device)
+    ws.gen += 1
+    si = torch.as_tensor(idx, dtype=torch.int64, device=dg.device)
+    sv = torch.as_tensor(val, dtype=torch.float64, device=dg.device)
+    hcap = _history_cap(geom)
+    hist = np.zeros(hcap, dtype=np.int64)
+    st = _native.Stats()
+    rc = _native.lib().eik_ifim_solve(
+        C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), _ptr(si), _ptr(sv), len(idx), float(tol),
+        ws.ptr, ws.nbytes, hist.ctypes.data_as(C.c_void_p), hcap, C.byref(st), dg.stream)
+    if dg.host:
+        _host_mark_sources(grid, idx)
+        dg.commit(phi=True)
+    _native.check(rc)
+    d = _stats_from(st)
+    stats = RunStats(
+        iterations=d["iterations"],
+        solver_calls=d["solver_calls"],
+        peak_active=d["peak_active"],
+        peak_remedy=d["peak_remedy"],
+        active_history=hist[: d["upd_iterations"]].tolist(),
+    )
+    stats.phi_writes = d["phi_writes"]
+    stats.phases = {
+        "update": {"iterations": d["upd_iterations"], "solver_calls": d["upd_calls"], "converged": d["converged"]},
+        "build": {"solver_calls": d["build_calls"], "remedy_size": d["remedy_size"]},
+        "remedy": {"iterations": d["rem_iterations"], "solver_calls": d["rem_calls"]},
+    }
+    stats.device_ms = {"update": d["upd_ms"], "build": d["build_ms"], "remedy": d["rem_ms"], "total": d["total_ms"]}
+    stats.gpu_launches = d["gpu_launches"]
+    stats.wall_time = time.perf_counter() - t0
+    phi = grid.phi.copy() if isinstance(grid.phi, np.ndarray) else grid.phi.clone()
+    return SolverResult(phi=phi, stats=stats)
