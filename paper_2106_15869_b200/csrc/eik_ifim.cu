@@ -72,9 +72,33 @@ struct Ctl {
     unsigned long long pad[3];
 };
 
+// Division by a runtime-invariant divisor for dividends < 2^31 (round-up
+// multiplier method): q = umulhi(n, mul) >> shr.
+struct FastDiv {
+    uint32_t d, mul, shr;
+};
+
+FastDiv make_fastdiv(uint32_t d)
+{
+    FastDiv f{d, 0u, 0u};
+    if (d <= 1) return f;
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;  // ceil(log2 d)
+    const uint32_t p = 31 + l;
+    f.mul = (uint32_t)(((1ull << p) + d - 1) / d);
+    f.shr = p - 32;
+    return f;
+}
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f)
+{
+    return f.d == 1 ? n : (__umulhi(n, f.mul) >> f.shr);
+}
+
 struct KP {
     int64_t nx, ny, nz, plane;
     uint32_t W, nwords, nrows, pad0;
+    FastDiv fnx, fny, fW;
     double dx, dy, delta, tol;
     double *P0, *P1;         // P0 = caller phi, P1 = workspace copy
     const double *F;         // speed
@@ -239,10 +263,10 @@ template <int DIM>
 __device__ __forceinline__ WPos wpos(const KP &p, uint32_t w)
 {
     WPos q;
-    q.row = w / p.W;
+    q.row = fdiv(w, p.fW);
     q.wx = w - q.row * p.W;
     if (DIM == 3) {
-        q.z = q.row / (uint32_t)p.ny;
+        q.z = fdiv(q.row, p.fny);
         q.y = q.row - q.z * (uint32_t)p.ny;
     } else {
         q.z = 0;
@@ -255,75 +279,100 @@ __device__ __forceinline__ WPos wpos(const KP &p, uint32_t w)
     return q;
 }
 
+// Jacobi snapshot around one cell (E/_kernels.py:29-38: out-of-grid reads
+// are +inf) plus the cell's coefficient (d = delta/F, or F for the
+// anisotropic solver).
 struct Sten {
-    double c, w, e, s, n, d, u;
+    double c, w, e, s, n, d, u, k;
+    double edge;  // word layout: lane 0 / lane 31 x-neighbour outside the word
 };
 
-// Gather the Jacobi snapshot around the lanes in `bits` (E/_kernels.py:29-38:
-// out-of-grid reads are +inf).  Lanes adjacent to an active lane also load
-// their own value so x-neighbours come from shuffles.
-template <int DIM>
-__device__ __forceinline__ void gather(const KP &p, const double *__restrict__ Pc, const WPos &q, uint32_t bits,
-                                       Sten &s)
+// Word layout, stage 1: issue every load of the word at once (one memory
+// round trip).  Lanes adjacent to an active lane load their own value so the
+// x-neighbours come from shuffles in stage 2.
+template <int DIM, int SOL>
+__device__ __forceinline__ void gather_issue(const KP &p, const double *__restrict__ Pc, const WPos &q, uint32_t bits,
+                                             Sten &s)
 {
     const unsigned lane = lane_id();
     const bool act = (bits >> lane) & 1u;
     const uint32_t need = (bits | (bits << 1) | (bits >> 1)) & q.rowm;
     const int64_t c = q.c0 + lane;
-    s.c = ((need >> lane) & 1u) ? ldcg(Pc + c) : INFINITY;
+    const double *pc = Pc + c;
+    s.c = s.edge = s.s = s.n = s.d = s.u = INFINITY;
+    s.k = 1.0;
+    if ((need >> lane) & 1u) s.c = ldcg(pc);
+    if (act) {
+        if (lane == 0 && q.wx > 0) s.edge = ldcg(pc - 1);
+        if (lane == 31 && q.x0 + 32 < p.nx) s.edge = ldcg(pc + 1);
+        if (q.y > 0) s.s = ldcg(pc - p.nx);
+        if (q.y + 1 < p.ny) s.n = ldcg(pc + p.nx);
+        if (DIM == 3) {
+            if (q.z > 0) s.d = ldcg(pc - p.plane);
+            if (q.z + 1 < p.nz) s.u = ldcg(pc + p.plane);
+        }
+        s.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
+    }
+}
+
+// Word layout, stage 2: x-neighbours by shuffle.
+__device__ __forceinline__ void gather_finish(const KP &p, const WPos &q, Sten &s)
+{
+    const unsigned lane = lane_id();
     double w = __shfl_up_sync(FULL, s.c, 1);
     double e = __shfl_down_sync(FULL, s.c, 1);
-    if (lane == 0) w = (act && q.wx > 0) ? ldcg(Pc + c - 1) : INFINITY;
-    if (lane == 31) e = (act && q.x0 + 32 < p.nx) ? ldcg(Pc + c + 1) : INFINITY;
+    if (lane == 0) w = s.edge;
+    if (lane == 31) e = s.edge;
     else if (q.x0 + lane + 1 >= p.nx) e = INFINITY;
     s.w = w;
     s.e = e;
-    s.s = s.n = s.d = s.u = INFINITY;
-    if (act) {
-        if (q.y > 0) s.s = ldcg(Pc + c - p.nx);
-        if (q.y + 1 < p.ny) s.n = ldcg(Pc + c + p.nx);
-        if (DIM == 3) {
-            if (q.z > 0) s.d = ldcg(Pc + c - p.plane);
-            if (q.z + 1 < p.nz) s.u = ldcg(Pc + c + p.plane);
-        }
-    }
+}
+
+template <int DIM, int SOL>
+__device__ __forceinline__ void gather(const KP &p, const double *__restrict__ Pc, const WPos &q, uint32_t bits,
+                                       Sten &s)
+{
+    gather_issue<DIM, SOL>(p, Pc, q, bits, s);
+    gather_finish(p, q, s);
 }
 
 // One local-solver call on the gathered stencil (E/ifim.py:57-59).
 template <int DIM, int SOL>
-__device__ __forceinline__ double solve(const KP &p, const Sten &s, int64_t c)
+__device__ __forceinline__ double solve(const KP &p, const Sten &s)
 {
     const double xm = dmin(s.w, s.e);
     const double ym = dmin(s.s, s.n);
-    if (SOL == SOL_U2) return upd2u(xm, ym, __ldg(p.dd + c));
-    if (SOL == SOL_A2) return upd2a(xm, ym, __ldg(p.F + c), p.dx, p.dy);
-    return upd3u(xm, ym, dmin(s.d, s.u), __ldg(p.dd + c), p.delta);
+    if (SOL == SOL_U2) return upd2u(xm, ym, s.k);
+    if (SOL == SOL_A2) return upd2a(xm, ym, s.k, p.dx, p.dy);
+    return upd3u(xm, ym, dmin(s.d, s.u), s.k, p.delta);
 }
 
-// Per-warp append buffer in shared memory -> global worklist.
-struct Appender {
-    uint32_t *buf;  // APPBUF entries (shared)
-    int n;          // warp-uniform fill
-};
-
-__device__ __forceinline__ void app_flush(Appender &a, uint32_t *glist, unsigned *glen)
+// Block-wide exclusive scan of a per-thread count plus one global reservation:
+// returns this thread's first slot in the global list whose length is *glen.
+__device__ __forceinline__ unsigned block_reserve(unsigned v, unsigned *glen, unsigned *sscan)
 {
-    __syncwarp();
-    if (a.n == 0) return;
-    unsigned base = 0;
-    if (lane_id() == 0) base = atomicAdd(glen, (unsigned)a.n);
-    base = __shfl_sync(FULL, base, 0);
-    for (int i = lane_id(); i < a.n; i += 32) glist[base + i] = a.buf[i];
-    __syncwarp();
-    a.n = 0;
-}
-
-__device__ __forceinline__ void app_push(Appender &a, bool want, uint32_t val, uint32_t *glist, unsigned *glen)
-{
-    const unsigned m = __ballot_sync(FULL, want);
-    if (want) a.buf[a.n + __popc(m & lanemask_lt())] = val;
-    a.n += __popc(m);
-    if (a.n > APPBUF - 32) app_flush(a, glist, glen);
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    unsigned inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(FULL, inc, o);
+        if (lane >= (unsigned)o) inc += t;
+    }
+    if (lane == 31) sscan[warp] = inc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned acc = 0;
+        for (int i = 0; i < WPB; ++i) {
+            const unsigned t = sscan[i];
+            sscan[i] = acc;
+            acc += t;
+        }
+        sscan[WPB] = acc ? atomicAdd(glen, acc) : 0u;
+    }
+    __syncthreads();
+    const unsigned pos = sscan[WPB] + sscan[warp] + inc - v;
+    __syncthreads();
+    return pos;
 }
 
 // ---------------------------------------------------------------------------
@@ -400,126 +449,113 @@ __global__ void k_init_active(KP p, const int64_t *seeds, int64_t nseeds)
             const uint32_t bit = 1u << (x & 31);
             const uint32_t old = atomicOr(p.Bt + w, bit);
             if (old & bit) continue;  // label != FAR
-            const uint32_t olda = atomicOr(p.B0 + w, bit);
-            if (olda == 0) p.L0[atomicAdd(&p.ctl->len[0], 1u)] = w;
-            atomicAdd(&p.ctl->cnt[0], 1ull);
+            p.L0[atomicAdd(&p.ctl->len[0], 1u)] = (uint32_t)e;
         }
     }
 }
 
 // ---------------------------------------------------------------------------
-// Update step: persistent kernel, one iteration per grid barrier
+// Update step: persistent kernel, one iteration per grid barrier.
+// The active list is a compacted list of cell indices processed one thread per
+// cell (a thin 3D wavefront leaves ~1 active cell per 32-cell row segment, so
+// a word layout would idle 31 of 32 lanes).  Next list = non-converged cells
+// + newly activated FAR neighbours; each cell enters it at most once (an
+// active cell is "touched", activation is an atomicOr on the touched bitmap),
+// so its length is exactly |A_{k+1}|.
 // ---------------------------------------------------------------------------
 
 template <int DIM, int SOL>
-__device__ __forceinline__ void upd_word(const KP &p, uint32_t w, const double *__restrict__ Pc, double *__restrict__ Pn,
-                                         uint32_t *Ac, uint32_t *An, uint32_t *Ln, unsigned *lenN, Appender &app,
-                                         unsigned long long &a_next, unsigned long long &a_writes,
-                                         unsigned long long &a_conv)
+__global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
 {
-    const unsigned lane = lane_id();
-    const uint32_t bits = ldcg(Ac + w);
-    __syncwarp();
-    if (lane == 0) Ac[w] = 0;  // consumed; this bitmap is the next-next one
-    const WPos q = wpos<DIM>(p, w);
-    Sten s;
-    gather<DIM>(p, Pc, q, bits, s);
-    const bool act = (bits >> lane) & 1u;
-    const int64_t c = q.c0 + lane;
-    double v = 0.0;
-    if (act) v = solve<DIM, SOL>(p, s, c);
-    // E/ifim.py:121: converged iff v == old or |v - old| <= tol
-    const bool conv = act && (v == s.c || fabs(v - s.c) <= p.tol);
-    const bool stay = act && !conv;
-    if (act) Pn[c] = stay ? v : s.c;  // E/ifim.py:128 (+ double-buffer carry)
-    const uint32_t stay_m = __ballot_sync(FULL, stay);
-    const uint32_t conv_m = __ballot_sync(FULL, conv);
-    if (lane == 0) {
-        a_writes += __popc(stay_m);
-        a_conv += __popc(conv_m);
-    }
-    // Activation of +inf, unblocked, FAR neighbours of converged cells (E/ifim.py:123-126).
-    const uint32_t inf_m = __ballot_sync(FULL, s.c == INFINITY);
-    const bool wcand = __ballot_sync(FULL, lane == 0 && conv && q.wx > 0 && s.w == INFINITY) != 0;
-    const bool ecand = __ballot_sync(FULL, lane == 31 && conv && q.x0 + 32 < p.nx && s.e == INFINITY) != 0;
-    const uint32_t cs = (q.y > 0) ? (conv_m & __ballot_sync(FULL, s.s == INFINITY)) : 0u;
-    const uint32_t cn = (q.y + 1 < p.ny) ? (conv_m & __ballot_sync(FULL, s.n == INFINITY)) : 0u;
-    uint32_t cd = 0, cu = 0;
-    if (DIM == 3) {
-        cd = (q.z > 0) ? (conv_m & __ballot_sync(FULL, s.d == INFINITY)) : 0u;
-        cu = (q.z + 1 < p.nz) ? (conv_m & __ballot_sync(FULL, s.u == INFINITY)) : 0u;
-    }
-    uint32_t cand = 0, extra = 0, tw = 0;
-    switch (lane) {
-        case 0: tw = w; cand = ((conv_m << 1) | (conv_m >> 1)) & inf_m & q.rowm; extra = stay_m; break;
-        case 1: tw = w - 1; cand = wcand ? 0x80000000u : 0u; break;
-        case 2: tw = w + 1; cand = ecand ? 1u : 0u; break;
-        case 3: tw = w - p.W; cand = cs; break;
-        case 4: tw = w + p.W; cand = cn; break;
-        case 5: tw = (uint32_t)(w - (uint32_t)p.ny * p.W); cand = cd; break;
-        case 6: tw = (uint32_t)(w + (uint32_t)p.ny * p.W); cand = cu; break;
-        default: break;
-    }
-    bool want = false;
-    if (cand | extra) {
-        uint32_t nb = 0;
-        if (cand) {
-            const uint32_t old = atomicOr(p.Bt + tw, cand);  // FAR -> ACTIVE exactly once
-            nb = cand & ~old;
-        }
-        const uint32_t setm = nb | extra;
-        if (setm) {
-            const uint32_t olda = atomicOr(An + tw, setm);
-            a_next += __popc(setm & ~olda);
-            want = (olda == 0);
-        }
-    }
-    app_push(app, want, tw, Ln, lenN);
-}
-
-template <int DIM, int SOL>
-__global__ void __launch_bounds__(BLOCK) k_update(KP p)
-{
-    __shared__ uint32_t sbuf[WPB][APPBUF];
+    __shared__ unsigned sscan[WPB + 1];
     __shared__ unsigned long long sred[WPB];
-    const unsigned warp = threadIdx.x >> 5;
-    const uint32_t gw = blockIdx.x * WPB + warp;
-    const uint32_t GW = gridDim.x * WPB;
     Ctl *ctl = p.ctl;
-    Appender app{sbuf[warp], 0};
     unsigned long long a_writes = 0, a_conv = 0;
-
-    const unsigned long long n0 = vload(&ctl->cnt[0]);
+    const unsigned n0 = vload(&ctl->len[0]);
     if (n0 == 0) return;  // no initial active cell: zero iterations
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         if (p.hist_cap > 0) p.hist[0] = (int64_t)n0;
         ctl->sum = n0;
         ctl->peak = n0;
     }
+    const uint32_t nx = (uint32_t)p.nx, ny = (uint32_t)p.ny, nz = (uint32_t)p.nz;
     for (int64_t it = 0;; ++it) {
         const int par = (int)(it & 1);
-        const double *Pc = par ? p.P1 : p.P0;
-        double *Pn = par ? p.P0 : p.P1;
-        uint32_t *Ac = par ? p.B1 : p.B0;
-        uint32_t *An = par ? p.B0 : p.B1;
-        const uint32_t *Lc = par ? p.L1 : p.L0;
+        const double *__restrict__ Pc = par ? p.P1 : p.P0;
+        double *__restrict__ Pn = par ? p.P0 : p.P1;
+        const uint32_t *__restrict__ Lc = par ? p.L1 : p.L0;
         uint32_t *Ln = par ? p.L0 : p.L1;
         unsigned *lenN = &ctl->len[(it + 1) % 3];
         const unsigned n = vload(&ctl->len[it % 3]);
-        unsigned long long a_next = 0;
-        for (uint32_t i = gw; i < n; i += GW)
-            upd_word<DIM, SOL>(p, ldcg(Lc + i), Pc, Pn, Ac, An, Ln, lenN, app, a_next, a_writes, a_conv);
-        app_flush(app, Ln, lenN);
-        const unsigned long long tot = block_sum(a_next, sred);
-        if (threadIdx.x == 0) {
-            if (tot) atomicAdd(&ctl->cnt[(it + 1) % 3], tot);
-            if (blockIdx.x == 0) {
-                ctl->len[(it + 2) % 3] = 0;
-                ctl->cnt[(it + 2) % 3] = 0;
+        for (unsigned base = blockIdx.x * BLOCK; base < n; base += gridDim.x * BLOCK) {
+            const unsigned i = base + threadIdx.x;
+            uint32_t c = 0, x = 0, y = 0, z = 0, r = 0;
+            unsigned emit = 0;  // bit 0: stay; bits 1..6: activate W, E, S, N, D, U
+            if (i < n) {
+                c = __ldcg(Lc + i);
+                r = fdiv(c, p.fnx);
+                x = c - r * nx;
+                if (DIM == 3) {
+                    z = fdiv(r, p.fny);
+                    y = r - z * ny;
+                } else {
+                    y = r;
+                }
+                const double *pc = Pc + c;
+                Sten s;
+                s.c = ldcg(pc);
+                s.w = x > 0 ? ldcg(pc - 1) : INFINITY;
+                s.e = x + 1 < nx ? ldcg(pc + 1) : INFINITY;
+                s.s = y > 0 ? ldcg(pc - p.nx) : INFINITY;
+                s.n = y + 1 < ny ? ldcg(pc + p.nx) : INFINITY;
+                s.d = s.u = INFINITY;
+                if (DIM == 3) {
+                    s.d = z > 0 ? ldcg(pc - p.plane) : INFINITY;
+                    s.u = z + 1 < nz ? ldcg(pc + p.plane) : INFINITY;
+                }
+                s.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
+                const double v = solve<DIM, SOL>(p, s);
+                // E/ifim.py:121: converged iff v == old or |v - old| <= tol
+                const bool conv = (v == s.c) || fabs(v - s.c) <= p.tol;
+                Pn[c] = conv ? s.c : v;  // E/ifim.py:128 (+ double-buffer carry)
+                if (!conv) {
+                    emit = 1u;
+                    ++a_writes;
+                } else {
+                    ++a_conv;
+                    // activate +inf, unblocked, FAR neighbours (E/ifim.py:123-126)
+                    const double nv[6] = {s.w, s.e, s.s, s.n, s.d, s.u};
+                    uint32_t old[6];
+#pragma unroll
+                    for (int k = 0; k < (DIM == 3 ? 6 : 4); ++k) {
+                        old[k] = 0xffffffffu;
+                        const bool inb = k == 0 ? x > 0 : k == 1 ? x + 1 < nx : k == 2 ? y > 0
+                                         : k == 3 ? y + 1 < ny : k == 4 ? z > 0 : z + 1 < nz;
+                        if (inb && nv[k] == INFINITY) {
+                            const uint32_t xe = k == 0 ? x - 1 : k == 1 ? x + 1 : x;
+                            const uint32_t re = k == 2 ? r - 1 : k == 3 ? r + 1 : k == 4 ? r - ny : k == 5 ? r + ny : r;
+                            const uint32_t bit = 1u << (xe & 31);
+                            old[k] = atomicOr(p.Bt + re * p.W + (xe >> 5), bit) | ~bit;
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < (DIM == 3 ? 6 : 4); ++k)
+                        if (old[k] != 0xffffffffu) emit |= 2u << k;
+                }
+            }
+            unsigned pos = block_reserve(__popc(emit), lenN, sscan);
+            if (emit & 1u) Ln[pos++] = c;
+#pragma unroll
+            for (int k = 0; k < (DIM == 3 ? 6 : 4); ++k) {
+                const int64_t off = k == 0 ? -1 : k == 1 ? 1 : k == 2 ? -p.nx : k == 3 ? p.nx : k == 4 ? -p.plane : p.plane;
+                if (emit & (2u << k)) Ln[pos++] = (uint32_t)((int64_t)c + off);
             }
         }
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctl->len[(it + 2) % 3] = 0;
+        }
         grid_barrier(ctl);
-        const unsigned long long m = vload(&ctl->cnt[(it + 1) % 3]);
+        const unsigned m = vload(&ctl->len[(it + 1) % 3]);
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             ctl->iters = it + 1;
             if (m) {
@@ -568,11 +604,11 @@ __global__ void __launch_bounds__(BLOCK) k_build(KP p, const double *__restrict_
         if (lane == 0) D0[w] = 0;
         if (freem == 0) continue;
         Sten s;
-        gather<DIM>(p, Pc, q, freem, s);
+        gather<DIM, SOL>(p, Pc, q, freem, s);
         const bool fr = (freem >> lane) & 1u;
         bool moved = false;
         if (fr) {
-            const double v = solve<DIM, SOL>(p, s, q.c0 + lane);
+            const double v = solve<DIM, SOL>(p, s);
             moved = fabs(v - s.c) > p.tol;  // NaN (inf - inf) is not flagged
         }
         const uint32_t mm = __ballot_sync(FULL, moved);
@@ -679,15 +715,17 @@ __device__ __forceinline__ void rem_phase_a(const KP &p, const uint2 *__restrict
 #pragma unroll
         for (int u = 0; u < REM_U; ++u) {
             q[u] = wpos<DIM>(p, e[u].x);
-            gather<DIM>(p, Pc, q[u], e[u].y, s[u]);
+            gather_issue<DIM, SOL>(p, Pc, q[u], e[u].y, s[u]);
         }
+#pragma unroll
+        for (int u = 0; u < REM_U; ++u) gather_finish(p, q[u], s[u]);
 #pragma unroll
         for (int u = 0; u < REM_U; ++u) {
             const bool act = (e[u].y >> lane) & 1u;
             const int64_t c = q[u].c0 + lane;
             bool dec = false;
             if (act) {
-                const double v = solve<DIM, SOL>(p, s[u], c);
+                const double v = solve<DIM, SOL>(p, s[u]);
                 dec = v < s[u].c - p.tol;  // E/ifim.py:203
                 Pn[c] = dec ? v : s[u].c;
             }
@@ -717,11 +755,11 @@ __device__ __forceinline__ void rem_phase_b(const KP &p, const uint32_t *__restr
             wv[k] = w;
             rv[k] = 0;
             if (w < p.nwords) {
-                const uint32_t row = w / p.W;
+                const uint32_t row = fdiv(w, p.fW);
                 const uint32_t wx = w - row * p.W;
                 uint32_t y, z;
                 if (DIM == 3) {
-                    z = row / (uint32_t)p.ny;
+                    z = fdiv(row, p.fny);
                     y = row - z * (uint32_t)p.ny;
                 } else {
                     z = 0;
@@ -747,36 +785,15 @@ __device__ __forceinline__ void rem_phase_b(const KP &p, const uint32_t *__restr
                 }
             }
         }
-        // block exclusive scan of cntf
-        unsigned v = cntf;
-        const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned t = __shfl_up_sync(FULL, v, o);
-            if (lane >= (unsigned)o) v += t;
-        }
-        if (lane == 31) sscan[warp] = v;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            unsigned acc = 0;
-            for (int i = 0; i < WPB; ++i) {
-                const unsigned t = sscan[i];
-                sscan[i] = acc;
-                acc += t;
-            }
-            sscan[WPB] = acc ? atomicAdd(lenN, acc) : 0u;
-        }
-        __syncthreads();
-        unsigned pos = sscan[WPB] + sscan[warp] + v - cntf;
+        unsigned pos = block_reserve(cntf, lenN, sscan);
 #pragma unroll
         for (int k = 0; k < PER; ++k)
             if (rv[k]) En[pos++] = make_uint2(wv[k], rv[k]);
-        __syncthreads();
     }
 }
 
 template <int DIM, int SOL>
-__global__ void __launch_bounds__(BLOCK) k_remedy(KP p, const unsigned *skip)
+__global__ void __launch_bounds__(BLOCK, 3) k_remedy(KP p, const unsigned *skip)
 {
     __shared__ unsigned long long sred[WPB];
     __shared__ unsigned sscan[WPB + 1];
@@ -892,7 +909,7 @@ int make_layout(const eik_geom *g, Layout &L)
     L.N = g->nx * g->ny * g->nz;
     const int64_t W = (g->nx + 31) / 32;
     const int64_t nw = W * g->ny * g->nz;
-    if (nw >= (int64_t)1 << 31 || L.N >= (int64_t)1 << 40) return fail(EIK_EINVAL, "grid too large");
+    if (L.N >= (int64_t)1 << 31) return fail(EIK_EINVAL, "grid too large: %lld cells (limit 2^31 per device)", (long long)L.N);
     L.W = (uint32_t)W;
     L.nwords = (uint32_t)nw;
     const int64_t s = g->nx + g->ny + (g->ndim == 3 ? g->nz : 0);
@@ -905,8 +922,9 @@ int make_layout(const eik_geom *g, Layout &L)
     L.off_b1 = o; o += al((size_t)nw * 4);
     L.off_bt = o; o += al((size_t)nw * 4);
     L.off_bf = o; o += al((size_t)nw * 4);
-    L.off_l0 = o; o += al((size_t)nw * 8);
-    L.off_l1 = o; o += al((size_t)nw * 8);
+    const size_t lst = std::max((size_t)L.N * 4, (size_t)nw * 8);  // cell list or (word, bits) list
+    L.off_l0 = o; o += al(lst);
+    L.off_l1 = o; o += al(lst);
     L.off_hist = o; o += al((size_t)(L.cap_upd + 2) * 8);
     L.off_ctl_u = o; o += al(sizeof(Ctl));
     L.off_ctl_r = o; o += al(sizeof(Ctl));
@@ -928,6 +946,9 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const doub
     memset(&p, 0, sizeof(p));
     p.nx = g->nx; p.ny = g->ny; p.nz = g->nz; p.plane = g->nx * g->ny;
     p.W = L.W; p.nwords = L.nwords; p.nrows = (uint32_t)(g->ny * g->nz);
+    p.fnx = make_fastdiv((uint32_t)g->nx);
+    p.fny = make_fastdiv((uint32_t)g->ny);
+    p.fW = make_fastdiv(L.W);
     p.dx = g->dx; p.dy = g->dy; p.delta = g->dx; p.tol = tol;
     p.P0 = phi;
     p.P1 = (double *)(b + L.off_phi2);
