@@ -48,7 +48,6 @@ namespace {
 constexpr unsigned FULL = 0xffffffffu;
 constexpr int BLOCK = 256;
 constexpr int WPB = BLOCK / 32;
-constexpr int APPBUF = 64;  // per-warp append buffer (entries)
 constexpr uint8_t ST_SOURCE = 2, ST_BLOCKED = 4;  // E/grid.py:21-26
 enum { SOL_U2 = 0, SOL_A2 = 1, SOL_U3 = 2 };
 
@@ -69,7 +68,7 @@ struct Ctl {
     unsigned long long iters;   // iterations / rounds executed
     unsigned long long free_cells;  // build: #free
     unsigned long long flagged;     // build: |R0|
-    unsigned long long pad[3];
+    unsigned long long dsum[3];     // remedy: |D_r| per rotating slot
 };
 
 // Division by a runtime-invariant divisor for dividends < 2^31 (round-up
@@ -98,19 +97,47 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f)
 struct KP {
     int64_t nx, ny, nz, plane;
     uint32_t W, nwords, nrows, pad0;
+    uint32_t nx32, plane32;  // cell indices are < 2^31 (make_layout)
     FastDiv fnx, fny, fW;
     double dx, dy, delta, tol;
     double *P0, *P1;         // P0 = caller phi, P1 = workspace copy
     const double *F;         // speed
     double *dd;              // delta / F (uniform solvers)
     const uint8_t *state;
-    uint32_t *B0, *B1, *Bt, *Bf;  // bitmaps: set A/B, touched, fixed (blocked|source)
-    uint32_t *L0, *L1;            // worklists (uint32 words or uint2 entries)
+    uint32_t *Bt;                 // touched bitmap (update step labels: not FAR)
+    uint32_t *L0, *L1;            // update-step cell worklists
     Ctl *ctl;
     int64_t *hist;
     int64_t hist_cap;
     int64_t cap;
+    // remedy bricks: 32 x TY x TZ cells, 64 row words per brick (tile-major bitmaps)
+    uint32_t ntx, nty, ntz, ntiles;
+    FastDiv fntx, fnty;
+    uint32_t *TR0, *TD0, *TD1, *TF;     // R0, D (double-buffered), fixed
+    uint32_t *TS0, *TS1, *TC;          // D round stamps (per parity), candidate stamps
+    uint32_t *TL0, *TL1;               // brick worklists
 };
+
+template <int DIM>
+struct Brick;
+template <>
+struct Brick<3> {
+    static constexpr int TY = 8, TZ = 8;
+};
+template <>
+struct Brick<2> {
+    static constexpr int TY = 64, TZ = 1;
+};
+constexpr int TROWS = 64;  // TY * TZ row words per brick
+
+template <int DIM>
+__device__ __forceinline__ uint32_t brick_row_index(const KP &p, uint32_t wx, uint32_t y, uint32_t z)
+{
+    constexpr int TY = Brick<DIM>::TY, TZ = Brick<DIM>::TZ;
+    const uint32_t T = ((z / TZ) * p.nty + y / TY) * p.ntx + wx;
+    return T * TROWS + (z % TZ) * TY + (y % TY);
+}
+
 
 // ---------------------------------------------------------------------------
 // Local solvers (bit-exact restatements; no FMA contraction)
@@ -157,44 +184,53 @@ __device__ __forceinline__ double upd2a(double a, double b, double f, double dx,
     return out;
 }
 
-// E/local_solver.py:91-157 (update_3d_uniform), verified branch walk; d = delta / f
+// E/local_solver.py:91-157 (update_3d_uniform), verified branch walk; d = delta / f.
+// Each branch's root is a pure function of the sorted neighbours and d, so the
+// three candidate roots are evaluated once, without divergence, and the
+// reference's walk (guard, demote/promote, visited set) then runs as predicate
+// logic over them.  Same expressions, same operation order: bit-identical.
 __device__ __forceinline__ double upd3u(double px, double py, double pz, double d, double delta)
 {
     double a1 = px, a2 = py, a3 = pz, t;
     if (a2 < a1) { t = a1; a1 = a2; a2 = t; }
     if (a3 < a2) { t = a2; a2 = a3; a3 = t; }
     if (a2 < a1) { t = a1; a1 = a2; a2 = t; }
-    if (a1 == INFINITY) return INFINITY;
+    // k = 1
+    const double r1 = a1 + d;
+    // k = 2 (E/local_solver.py:136-151)
+    const double diff = a2 - a1;
+    const double disc2 = 2.0 * d * d - diff * diff;
+    const bool fail2 = (a2 == INFINITY) || (disc2 < -DISC_CLAMP * (2.0 * d * d));
+    const double r2 = 0.5 * (a1 + a2 + sqrt(disc2 > 0.0 ? disc2 : 0.0));
+    // k = 3 (E/local_solver.py:119-134)
+    const double b3 = a3 - a1;
+    const double s3 = diff + b3;
+    const double disc3 = s3 * s3 - 3.0 * (diff * diff + b3 * b3 - d * d);
+    const bool fail3 = disc3 < -DISC_CLAMP * (3.0 * d * d);
+    const double r3 = a1 + (s3 + sqrt(disc3 > 0.0 ? disc3 : 0.0)) / 3.0;
     int k = (a3 - a1 < delta) ? 3 : ((a2 - a1 < delta) ? 2 : 1);
-    unsigned visited = 0;
+    unsigned vis = 0;
+    double out = r1;
 #pragma unroll 1
-    for (int guard = 0; guard < 8; ++guard) {
-        visited |= 1u << k;
+    for (int step = 0; step < 8; ++step) {
+        vis |= 1u << k;
         if (k == 3) {
-            const double b2 = a2 - a1;
-            const double b3 = a3 - a1;
-            const double s = b2 + b3;
-            const double disc = s * s - 3.0 * (b2 * b2 + b3 * b3 - d * d);
-            if (disc < -DISC_CLAMP * (3.0 * d * d)) { k = 2; continue; }
-            const double root = a1 + (s + sqrt(disc > 0.0 ? disc : 0.0)) / 3.0;
-            if (root >= a3 || (visited & 4u)) return root;
+            if (fail3) { k = 2; continue; }
+            if (r3 >= a3 || (vis & 4u)) { out = r3; break; }
             k = 2;
         } else if (k == 2) {
-            if (a2 == INFINITY) { k = 1; continue; }
-            const double diff = a2 - a1;
-            const double disc = 2.0 * d * d - diff * diff;
-            if (disc < -DISC_CLAMP * (2.0 * d * d)) { k = 1; continue; }
-            const double root = 0.5 * (a1 + a2 + sqrt(disc > 0.0 ? disc : 0.0));
-            if (root < a2 && !(visited & 2u)) { k = 1; continue; }
-            if (root > a3 && !(visited & 8u)) { k = 3; continue; }
-            return root;
+            if (fail2) { k = 1; continue; }
+            if (r2 < a2 && !(vis & 2u)) { k = 1; continue; }
+            if (r2 > a3 && !(vis & 8u)) { k = 3; continue; }
+            out = r2;
+            break;
         } else {
-            const double root = a1 + d;
-            if (root > a2 && !(visited & 4u)) { k = 2; continue; }
-            return root;
+            if (r1 > a2 && !(vis & 4u)) { k = 2; continue; }
+            out = r1;
+            break;
         }
     }
-    return NAN;  // unreachable: the walk visits each branch at most twice
+    return a1 == INFINITY ? INFINITY : out;
 }
 
 // ---------------------------------------------------------------------------
@@ -202,32 +238,53 @@ __device__ __forceinline__ double upd3u(double px, double py, double pz, double 
 // ---------------------------------------------------------------------------
 
 __device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
-__device__ __forceinline__ uint32_t ldcg(const uint32_t *p) { return __ldcg(p); }
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
-__device__ __forceinline__ unsigned lanemask_lt() { return (1u << lane_id()) - 1u; }
 
 template <typename T>
 __device__ __forceinline__ T vload(const T *p) { return *(const volatile T *)p; }
 
-// Software grid barrier; all CTAs are co-resident (cooperative launch).
-__device__ __forceinline__ void grid_barrier(Ctl *ctl)
+__device__ __forceinline__ unsigned long long globaltimer()
 {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+constexpr unsigned EIK_EHANG = 5;  // device-side watchdog tripped (reported as a CUDA error)
+
+// Software grid barrier; all CTAs are co-resident (cooperative launch).
+// Returns false if the watchdog fired (a CTA did not arrive within ~10 s);
+// every caller then leaves the kernel so a logic error cannot wedge the GPU.
+__device__ __forceinline__ bool grid_barrier(Ctl *ctl)
+{
+    __shared__ unsigned s_ok;
     __syncthreads();
     if (threadIdx.x == 0) {
         volatile unsigned *vgen = &ctl->bar_gen;
         const unsigned gen = *vgen;
         __threadfence();
         const unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
+        unsigned ok = 1;
         if (arrived == gridDim.x - 1) {
             atomicExch(&ctl->bar_count, 0u);
             __threadfence();
             atomicAdd(&ctl->bar_gen, 1u);
         } else {
-            while (*vgen == gen) { __nanosleep(32); }
+            const unsigned long long t0 = globaltimer();
+            while (*vgen == gen) {
+                __nanosleep(32);
+                if (*(volatile unsigned *)&ctl->err == EIK_EHANG || globaltimer() - t0 > 10000000000ull) {
+                    atomicExch(&ctl->err, EIK_EHANG);
+                    ok = 0;
+                    break;
+                }
+            }
         }
         __threadfence();
+        s_ok = ok && *(volatile unsigned *)&ctl->err != EIK_EHANG;
     }
     __syncthreads();
+    return s_ok != 0;
 }
 
 template <typename T>
@@ -255,7 +312,7 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, un
 
 struct WPos {
     uint32_t row, wx, y, z;
-    int64_t x0, c0;
+    uint32_t x0, c0;
     uint32_t rowm;  // lanes inside the row
 };
 
@@ -272,9 +329,9 @@ __device__ __forceinline__ WPos wpos(const KP &p, uint32_t w)
         q.z = 0;
         q.y = q.row;
     }
-    q.x0 = (int64_t)q.wx * 32;
-    q.c0 = (int64_t)q.row * p.nx + q.x0;
-    const int64_t nv = p.nx - q.x0;
+    q.x0 = q.wx * 32u;
+    q.c0 = q.row * p.nx32 + q.x0;
+    const uint32_t nv = p.nx32 - q.x0;
     q.rowm = nv >= 32 ? FULL : ((1u << nv) - 1u);
     return q;
 }
@@ -297,19 +354,18 @@ __device__ __forceinline__ void gather_issue(const KP &p, const double *__restri
     const unsigned lane = lane_id();
     const bool act = (bits >> lane) & 1u;
     const uint32_t need = (bits | (bits << 1) | (bits >> 1)) & q.rowm;
-    const int64_t c = q.c0 + lane;
-    const double *pc = Pc + c;
+    const uint32_t c = q.c0 + lane;
     s.c = s.edge = s.s = s.n = s.d = s.u = INFINITY;
     s.k = 1.0;
-    if ((need >> lane) & 1u) s.c = ldcg(pc);
+    if ((need >> lane) & 1u) s.c = ldcg(Pc + c);
     if (act) {
-        if (lane == 0 && q.wx > 0) s.edge = ldcg(pc - 1);
-        if (lane == 31 && q.x0 + 32 < p.nx) s.edge = ldcg(pc + 1);
-        if (q.y > 0) s.s = ldcg(pc - p.nx);
-        if (q.y + 1 < p.ny) s.n = ldcg(pc + p.nx);
+        if (lane == 0 && q.wx > 0) s.edge = ldcg(Pc + (c - 1));
+        if (lane == 31 && q.x0 + 32 < p.nx32) s.edge = ldcg(Pc + (c + 1));
+        if (q.y > 0) s.s = ldcg(Pc + (c - p.nx32));
+        if (q.y + 1 < p.ny) s.n = ldcg(Pc + (c + p.nx32));
         if (DIM == 3) {
-            if (q.z > 0) s.d = ldcg(pc - p.plane);
-            if (q.z + 1 < p.nz) s.u = ldcg(pc + p.plane);
+            if (q.z > 0) s.d = ldcg(Pc + (c - p.plane32));
+            if (q.z + 1 < p.nz) s.u = ldcg(Pc + (c + p.plane32));
         }
         s.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
     }
@@ -323,7 +379,7 @@ __device__ __forceinline__ void gather_finish(const KP &p, const WPos &q, Sten &
     double e = __shfl_down_sync(FULL, s.c, 1);
     if (lane == 0) w = s.edge;
     if (lane == 31) e = s.edge;
-    else if (q.x0 + lane + 1 >= p.nx) e = INFINITY;
+    else if (q.x0 + lane + 1 >= p.nx32) e = INFINITY;
     s.w = w;
     s.e = e;
 }
@@ -390,18 +446,16 @@ __global__ void k_seed(double *phi, uint8_t *state, const int64_t *idx, const do
 
 // One pass over all words: copy phi into the second buffer, d = delta / F,
 // touched = blocked, fixed = blocked | source, optionally clear set bitmaps.
-template <bool UNIFORM>
-__global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_touched, uint32_t *clr0,
-                                                uint32_t *clr1)
+template <int DIM, bool UNIFORM>
+__global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_touched)
 {
     const unsigned lane = lane_id();
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t w = gw; w < p.nwords; w += GW) {
-        const uint32_t row = w / p.W;
-        const int64_t x = (int64_t)(w - row * p.W) * 32 + lane;
-        const bool in = x < p.nx;
-        const int64_t c = (int64_t)row * p.nx + x;
+        const WPos q = wpos<DIM>(p, w);
+        const bool in = (q.rowm >> lane) & 1u;
+        const uint32_t c = q.c0 + lane;
         uint8_t st = 0;
         if (in) {
             st = p.state[c];
@@ -411,10 +465,8 @@ __global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_
         const uint32_t blk = __ballot_sync(FULL, in && st == ST_BLOCKED);
         const uint32_t src = __ballot_sync(FULL, in && st == ST_SOURCE);
         if (lane == 0) {
-            p.Bf[w] = blk | src;
+            p.TF[brick_row_index<DIM>(p, q.wx, q.y, q.z)] = blk | src | ~q.rowm;  // out-of-grid lanes are fixed
             if (build_touched) p.Bt[w] = blk;
-            if (clr0) clr0[w] = 0;
-            if (clr1) clr1[w] = 0;
         }
     }
 }
@@ -501,17 +553,16 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
                 } else {
                     y = r;
                 }
-                const double *pc = Pc + c;
                 Sten s;
-                s.c = ldcg(pc);
-                s.w = x > 0 ? ldcg(pc - 1) : INFINITY;
-                s.e = x + 1 < nx ? ldcg(pc + 1) : INFINITY;
-                s.s = y > 0 ? ldcg(pc - p.nx) : INFINITY;
-                s.n = y + 1 < ny ? ldcg(pc + p.nx) : INFINITY;
+                s.c = ldcg(Pc + c);
+                s.w = x > 0 ? ldcg(Pc + (c - 1)) : INFINITY;
+                s.e = x + 1 < nx ? ldcg(Pc + (c + 1)) : INFINITY;
+                s.s = y > 0 ? ldcg(Pc + (c - nx)) : INFINITY;
+                s.n = y + 1 < ny ? ldcg(Pc + (c + nx)) : INFINITY;
                 s.d = s.u = INFINITY;
                 if (DIM == 3) {
-                    s.d = z > 0 ? ldcg(pc - p.plane) : INFINITY;
-                    s.u = z + 1 < nz ? ldcg(pc + p.plane) : INFINITY;
+                    s.d = z > 0 ? ldcg(Pc + (c - p.plane32)) : INFINITY;
+                    s.u = z + 1 < nz ? ldcg(Pc + (c + p.plane32)) : INFINITY;
                 }
                 s.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
                 const double v = solve<DIM, SOL>(p, s);
@@ -547,14 +598,15 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
             if (emit & 1u) Ln[pos++] = c;
 #pragma unroll
             for (int k = 0; k < (DIM == 3 ? 6 : 4); ++k) {
-                const int64_t off = k == 0 ? -1 : k == 1 ? 1 : k == 2 ? -p.nx : k == 3 ? p.nx : k == 4 ? -p.plane : p.plane;
-                if (emit & (2u << k)) Ln[pos++] = (uint32_t)((int64_t)c + off);
+                const uint32_t e = k == 0 ? c - 1 : k == 1 ? c + 1 : k == 2 ? c - nx : k == 3 ? c + nx
+                                   : k == 4 ? c - p.plane32 : c + p.plane32;
+                if (emit & (2u << k)) Ln[pos++] = e;
             }
         }
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             ctl->len[(it + 2) % 3] = 0;
         }
-        grid_barrier(ctl);
+        if (!grid_barrier(ctl)) return;
         const unsigned m = vload(&ctl->len[(it + 1) % 3]);
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             ctl->iters = it + 1;
@@ -579,271 +631,329 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
 }
 
 // ---------------------------------------------------------------------------
+// Brick helpers.  Brick T = (tz * nty + ty) * ntx + tx covers x in
+// [32 tx, 32 tx + 32), y in [TY ty, ...), z in [TZ tz, ...); its 64 row words
+// live at T * 64 + (z % TZ) * TY + (y % TY) in every tile-major bitmap.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void push_brick(const KP &p, uint32_t T, uint32_t stamp, uint32_t *list, unsigned *len)
+{
+    if (atomicExch(p.TC + T, stamp) != stamp) list[atomicAdd(len, 1u)] = T;
+}
+
+// ---------------------------------------------------------------------------
 // Build pass (E/ifim.py:137-161): one value per free cell, flag |v - phi| > tol.
-// Writes the remedy list R0 as (word, bits) entries and zeroes D[0].
+// Writes R0 into the tile-major bitmap and the list of bricks holding it.
 // ---------------------------------------------------------------------------
 
 template <int DIM, int SOL>
-__global__ void __launch_bounds__(BLOCK) k_build(KP p, const double *__restrict__ Pc, uint2 *E0, uint32_t *D0,
-                                                 const unsigned *skip)
+__global__ void __launch_bounds__(BLOCK) k_build(KP p, const double *__restrict__ Pc, const unsigned *skip)
 {
-    __shared__ uint32_t sbuf[WPB][APPBUF];
-    __shared__ uint32_t sbits[WPB][APPBUF];
     __shared__ unsigned long long sred[WPB];
     if (skip && *skip) return;
     const unsigned lane = lane_id();
-    const unsigned warp = threadIdx.x >> 5;
-    const uint32_t gw = blockIdx.x * WPB + warp;
-    const uint32_t GW = gridDim.x * WPB;
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
     Ctl *ctl = p.ctl;
-    int nb = 0;
     unsigned long long a_free = 0, a_flag = 0;
     for (uint32_t w = gw; w < p.nwords; w += GW) {
         const WPos q = wpos<DIM>(p, w);
-        const uint32_t freem = q.rowm & ~__ldg(p.Bf + w);
-        if (lane == 0) D0[w] = 0;
+        const uint32_t ri = brick_row_index<DIM>(p, q.wx, q.y, q.z);
+        const uint32_t freem = q.rowm & ~__ldg(p.TF + ri);
         if (freem == 0) continue;
         Sten s;
         gather<DIM, SOL>(p, Pc, q, freem, s);
-        const bool fr = (freem >> lane) & 1u;
         bool moved = false;
-        if (fr) {
+        if ((freem >> lane) & 1u) {
             const double v = solve<DIM, SOL>(p, s);
             moved = fabs(v - s.c) > p.tol;  // NaN (inf - inf) is not flagged
         }
         const uint32_t mm = __ballot_sync(FULL, moved);
         if (lane == 0) {
             a_free += __popc(freem);
-            a_flag += __popc(mm);
-        }
-        if (mm) {
-            if (lane == 0) {
-                sbuf[warp][nb] = w;
-                sbits[warp][nb] = mm;
-            }
-            ++nb;
-            if (nb == APPBUF) {
-                __syncwarp();
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(&ctl->len[0], (unsigned)nb);
-                base = __shfl_sync(FULL, base, 0);
-                for (int i = lane; i < nb; i += 32) E0[base + i] = make_uint2(sbuf[warp][i], sbits[warp][i]);
-                __syncwarp();
-                nb = 0;
+            if (mm) {
+                a_flag += __popc(mm);
+                p.TR0[ri] = mm;
+                push_brick(p, ri / TROWS, 0u, p.TL0, &ctl->len[0]);
             }
         }
-    }
-    __syncwarp();
-    if (nb) {
-        unsigned base = 0;
-        if (lane == 0) base = atomicAdd(&ctl->len[0], (unsigned)nb);
-        base = __shfl_sync(FULL, base, 0);
-        for (int i = lane; i < nb; i += 32) E0[base + i] = make_uint2(sbuf[warp][i], sbits[warp][i]);
     }
     const unsigned long long tf = block_sum(a_free, sred);
     const unsigned long long tg = block_sum(a_flag, sred);
     if (threadIdx.x == 0) {
         atomicAdd(&ctl->free_cells, tf);
         atomicAdd(&ctl->flagged, tg);
-        atomicAdd(&ctl->cnt[0], tg);
     }
 }
 
-// Remedy set from a uint8 mask (RemedySet.member), zeroing D[0].
-__global__ void __launch_bounds__(BLOCK) k_remedy_load(KP p, const uint8_t *member, uint2 *E0, uint32_t *D0)
+// Remedy set from a uint8 mask (a RemedySet built elsewhere).
+template <int DIM>
+__global__ void __launch_bounds__(BLOCK) k_remedy_load(KP p, const uint8_t *member)
 {
     const unsigned lane = lane_id();
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
     unsigned long long cnt = 0;
     for (uint32_t w = gw; w < p.nwords; w += GW) {
-        const uint32_t row = w / p.W;
-        const int64_t x = (int64_t)(w - row * p.W) * 32 + lane;
-        const bool in = x < p.nx;
-        const int64_t c = (int64_t)row * p.nx + x;
-        const uint32_t m = __ballot_sync(FULL, in && member[c] != 0);
-        if (lane == 0) {
-            D0[w] = 0;
-            if (m) {
-                E0[atomicAdd(&p.ctl->len[0], 1u)] = make_uint2(w, m);
-                cnt += __popc(m);
-            }
+        const WPos q = wpos<DIM>(p, w);
+        const bool in = (q.rowm >> lane) & 1u;
+        const uint32_t m = __ballot_sync(FULL, in && member[q.c0 + lane] != 0);
+        if (lane == 0 && m) {
+            const uint32_t ri = brick_row_index<DIM>(p, q.wx, q.y, q.z);
+            p.TR0[ri] = m;
+            push_brick(p, ri / TROWS, 0u, p.TL0, &p.ctl->len[0]);
+            cnt += __popc(m);
         }
     }
-    if (lane == 0 && cnt) atomicAdd(&p.ctl->cnt[0], cnt);
-}
-
-__global__ void k_remedy_export(KP p, const uint2 *E0, unsigned n, uint8_t *member)
-{
-    const unsigned lane = lane_id();
-    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
-    for (uint32_t i = gw; i < n; i += GW) {
-        const uint2 e = E0[i];
-        const uint32_t row = e.x / p.W;
-        const int64_t x = (int64_t)(e.x - row * p.W) * 32 + lane;
-        if ((e.y >> lane) & 1u) member[(int64_t)row * p.nx + x] = 1;
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Remedy step: persistent kernel, two phases per round.
-//   A: for every (word, bits) of R_r: v = U(snapshot); D_r = {v < phi - tol};
-//      write P_next (E/ifim.py:199-208).
-//   B: R_{r+1} = D_r | (N(D_r) & ~fixed), one thread per word over the whole
-//      bitmap (E/ifim.py:209-214, set form: membership only dedups), compacted
-//      into the next (word, bits) list.
-// ---------------------------------------------------------------------------
-
-constexpr int REM_U = 2;  // words in flight per warp in phase A
-
-template <int DIM, int SOL>
-__device__ __forceinline__ void rem_phase_a(const KP &p, const uint2 *__restrict__ Ec, unsigned n,
-                                            const double *__restrict__ Pc, double *__restrict__ Pn, uint32_t *Dc,
-                                            unsigned long long &a_dec, uint32_t gw, uint32_t GW)
-{
-    const unsigned lane = lane_id();
-    for (uint32_t base = gw * REM_U; base < n; base += GW * REM_U) {
-        uint2 e[REM_U];
-        WPos q[REM_U];
-        Sten s[REM_U];
-#pragma unroll
-        for (int u = 0; u < REM_U; ++u) {
-            const uint32_t i = base + u;
-            e[u] = (i < n) ? __ldcg(Ec + i) : make_uint2(0u, 0u);
-        }
-#pragma unroll
-        for (int u = 0; u < REM_U; ++u) {
-            q[u] = wpos<DIM>(p, e[u].x);
-            gather_issue<DIM, SOL>(p, Pc, q[u], e[u].y, s[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < REM_U; ++u) gather_finish(p, q[u], s[u]);
-#pragma unroll
-        for (int u = 0; u < REM_U; ++u) {
-            const bool act = (e[u].y >> lane) & 1u;
-            const int64_t c = q[u].c0 + lane;
-            bool dec = false;
-            if (act) {
-                const double v = solve<DIM, SOL>(p, s[u]);
-                dec = v < s[u].c - p.tol;  // E/ifim.py:203
-                Pn[c] = dec ? v : s[u].c;
-            }
-            const uint32_t dm = __ballot_sync(FULL, dec);
-            if (lane == 0 && e[u].y) {
-                Dc[e[u].x] = dm;
-                a_dec += __popc(dm);
-            }
-        }
-    }
+    if (lane == 0 && cnt) atomicAdd(&p.ctl->flagged, cnt);
 }
 
 template <int DIM>
-__device__ __forceinline__ void rem_phase_b(const KP &p, const uint32_t *__restrict__ Dc, uint32_t *Dn, uint2 *En,
-                                            unsigned *lenN, unsigned long long &a_next, unsigned *sscan)
+__global__ void k_remedy_export(KP p, unsigned n, uint8_t *member)
 {
-    // chunks of BLOCK*4 words per block, thread t takes words base + t + k*BLOCK
-    constexpr int PER = 4;
-    const uint32_t chunk = BLOCK * PER;
-    const uint32_t planeW = (uint32_t)p.ny * p.W;
-    for (uint32_t base = blockIdx.x * chunk; base < p.nwords; base += gridDim.x * chunk) {
-        uint32_t wv[PER], rv[PER];
-        int cntf = 0;
-#pragma unroll
-        for (int k = 0; k < PER; ++k) {
-            const uint32_t w = base + threadIdx.x + k * BLOCK;
-            wv[k] = w;
-            rv[k] = 0;
-            if (w < p.nwords) {
-                const uint32_t row = fdiv(w, p.fW);
-                const uint32_t wx = w - row * p.W;
-                uint32_t y, z;
-                if (DIM == 3) {
-                    z = fdiv(row, p.fny);
-                    y = row - z * (uint32_t)p.ny;
-                } else {
-                    z = 0;
-                    y = row;
-                }
-                const uint32_t c = ldcg(Dc + w);
-                uint32_t dil = (c << 1) | (c >> 1);
-                if (wx > 0) dil |= ldcg(Dc + w - 1) >> 31;
-                if (wx + 1 < p.W) dil |= ldcg(Dc + w + 1) << 31;
-                if (y > 0) dil |= ldcg(Dc + w - p.W);
-                if (y + 1 < p.ny) dil |= ldcg(Dc + w + p.W);
-                if (DIM == 3) {
-                    if (z > 0) dil |= ldcg(Dc + w - planeW);
-                    if (z + 1 < p.nz) dil |= ldcg(Dc + w + planeW);
-                }
-                const int64_t nv = p.nx - (int64_t)wx * 32;
-                const uint32_t rowm = nv >= 32 ? FULL : ((1u << nv) - 1u);
-                rv[k] = (c | (dil & ~__ldg(p.Bf + w))) & rowm;
-                Dn[w] = 0;  // D_{r+1} is written sparsely by the next phase A
-                if (rv[k]) {
-                    ++cntf;
-                    a_next += __popc(rv[k]);
-                }
+    constexpr int TY = Brick<DIM>::TY;
+    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
+        const uint32_t T = p.TL0[i];
+        const uint32_t t1 = fdiv(T, p.fntx), tx = T - t1 * p.ntx;
+        const uint32_t tz = fdiv(t1, p.fnty), ty = t1 - tz * p.nty;
+        for (uint32_t e = threadIdx.x; e < TROWS * 32; e += blockDim.x) {
+            const uint32_t row = e >> 5, x = e & 31;
+            if ((p.TR0[T * TROWS + row] >> x) & 1u) {
+                const uint32_t gx = tx * 32 + x, gy = ty * TY + row % TY, gz = tz * Brick<DIM>::TZ + row / TY;
+                member[(gz * (uint32_t)p.ny + gy) * p.nx32 + gx] = 1;
             }
         }
-        unsigned pos = block_reserve(cntf, lenN, sscan);
-#pragma unroll
-        for (int k = 0; k < PER; ++k)
-            if (rv[k]) En[pos++] = make_uint2(wv[k], rv[k]);
     }
 }
+
+// ---------------------------------------------------------------------------
+// Remedy step (E/ifim.py:164-218): persistent kernel, one grid barrier per
+// round, one brick per CTA at a time.
+//
+// Round r processes the candidate bricks of the round:
+//   1. R_r(brick): round 0 reads R0; later rounds pull
+//      R_r = D_{r-1} | (N(D_{r-1}) & ~fixed) from the brick's own and its six
+//      face neighbours' D_{r-1} words (D words are valid only if the brick's
+//      round stamp says r-1, so no bitmap is ever cleared).
+//   2. phi of the brick plus a one-cell halo is staged in shared memory
+//      (out-of-grid halo = +inf, E/_kernels.py:21-26).
+//   3. Members are compacted so every lane runs a local solve; v < phi - tol
+//      writes P_next and sets the D bit (E/ifim.py:199-208).
+//   4. D_r(brick) is published with its stamp; if non-empty the brick and the
+//      face neighbours its decreases touch become candidates of round r+1
+//      (E/ifim.py:209-213, set form).
+// |R_r| and |D_r| are counted exactly; the loop ends when D_r is empty.
+// ---------------------------------------------------------------------------
 
 template <int DIM, int SOL>
 __global__ void __launch_bounds__(BLOCK, 3) k_remedy(KP p, const unsigned *skip)
 {
+    constexpr int TY = Brick<DIM>::TY, TZ = Brick<DIM>::TZ;
+    constexpr int HX = 34, HY = TY + 2, HZ = DIM == 3 ? TZ + 2 : 1;
+    constexpr int HN = HX * HY * HZ;
+    constexpr int HZS = HX * HY;  // halo z stride
+    __shared__ double halo[HN];
+    __shared__ uint32_t sR[TROWS], sD[TROWS];
+    __shared__ uint16_t mlist[TROWS * 32];
+    __shared__ unsigned sscan[2], soff[TROWS];
+    __shared__ unsigned s_flags;
     __shared__ unsigned long long sred[WPB];
-    __shared__ unsigned sscan[WPB + 1];
     if (skip && *skip) return;
-    const unsigned warp = threadIdx.x >> 5;
-    const uint32_t gw = blockIdx.x * WPB + warp;
-    const uint32_t GW = gridDim.x * WPB;
     Ctl *ctl = p.ctl;
-    unsigned long long a_dec = 0;
-    const unsigned long long r0 = vload(&ctl->cnt[0]);
+    const unsigned tid = threadIdx.x, lane = lane_id();
+    const unsigned long long r0 = vload(&ctl->flagged);
     if (r0 == 0) return;  // empty remedy set: zero rounds
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blockIdx.x == 0 && tid == 0) {
         ctl->peak = r0;
         ctl->sum = 0;
     }
-    const uint2 *E[2] = {reinterpret_cast<const uint2 *>(p.L0), reinterpret_cast<const uint2 *>(p.L1)};
-    for (int64_t r = 0;; ++r) {
+    if (tid == 0) s_flags = 0;
+    const uint32_t nx = p.nx32, ny = (uint32_t)p.ny, nz = (uint32_t)p.nz;
+    for (uint32_t r = 0;; ++r) {
         const int par = (int)(r & 1);
-        const double *Pc = par ? p.P1 : p.P0;
-        double *Pn = par ? p.P0 : p.P1;
-        uint32_t *Dc = par ? p.B1 : p.B0;
-        uint32_t *Dn = par ? p.B0 : p.B1;
+        const double *__restrict__ Pc = par ? p.P1 : p.P0;
+        double *__restrict__ Pn = par ? p.P0 : p.P1;
+        uint32_t *Dc = par ? p.TD1 : p.TD0;
+        const uint32_t *Dp = par ? p.TD0 : p.TD1;
+        uint32_t *Sc = par ? p.TS1 : p.TS0;
+        const uint32_t *Sp = par ? p.TS0 : p.TS1;
+        const uint32_t *TLc = par ? p.TL1 : p.TL0;
+        uint32_t *TLn = par ? p.TL0 : p.TL1;
+        unsigned *lenN = &ctl->len[(r + 1) % 3];
         const unsigned n = vload(&ctl->len[r % 3]);
-        rem_phase_a<DIM, SOL>(p, E[par], n, Pc, Pn, Dc, a_dec, gw, GW);
-        grid_barrier(ctl);
-        unsigned long long a_next = 0;
-        rem_phase_b<DIM>(p, Dc, Dn, const_cast<uint2 *>(E[par ^ 1]), &ctl->len[(r + 1) % 3], a_next, sscan);
-        const unsigned long long tot = block_sum(a_next, sred);
-        if (threadIdx.x == 0) {
-            if (tot) atomicAdd(&ctl->cnt[(r + 1) % 3], tot);
+        unsigned long long a_calls = 0, a_dec = 0;
+        for (unsigned ti = blockIdx.x; ti < n; ti += gridDim.x) {
+            const uint32_t T = __ldcg(TLc + ti);
+            const uint32_t t1 = fdiv(T, p.fntx), tx = T - t1 * p.ntx;
+            const uint32_t tz = fdiv(t1, p.fnty), ty = t1 - tz * p.nty;
+            const uint32_t x0 = tx * 32, y0 = ty * TY, z0 = tz * TZ;
+            // (2) stage phi + halo
+            for (unsigned i = tid; i < (unsigned)HN; i += BLOCK) {
+                const unsigned hx = i % HX, hy = (i / HX) % HY, hz = i / HZS;
+                const int gx = (int)(x0 + hx) - 1, gy = (int)(y0 + hy) - 1;
+                const int gz = DIM == 3 ? (int)(z0 + hz) - 1 : 0;
+                double v = INFINITY;
+                if (gx >= 0 && gx < (int)nx && gy >= 0 && gy < (int)ny && gz >= 0 && gz < (int)nz)
+                    v = ldcg(Pc + (((uint32_t)gz * ny + (uint32_t)gy) * nx + (uint32_t)gx));
+                halo[i] = v;
+            }
+            // (1) R_r of this brick
+            if (tid < TROWS) {
+                const uint32_t row = tid, yl = row % TY, zl = row / TY;
+                const uint32_t base = T * TROWS;
+                uint32_t R;
+                if (r == 0) {
+                    R = __ldcg(p.TR0 + base + row);
+                } else {
+                    const uint32_t want = r - 1;
+                    const bool own = __ldcg(Sp + T) == want;
+                    const uint32_t c = own ? __ldcg(Dp + base + row) : 0u;
+                    uint32_t dil = (c << 1) | (c >> 1);
+                    if (tx > 0 && __ldcg(Sp + T - 1) == want) dil |= __ldcg(Dp + base - TROWS + row) >> 31;
+                    if (tx + 1 < p.ntx && __ldcg(Sp + T + 1) == want) dil |= __ldcg(Dp + base + TROWS + row) << 31;
+                    if (yl > 0) {
+                        if (own) dil |= __ldcg(Dp + base + row - 1);
+                    } else if (ty > 0) {
+                        const uint32_t Tn = T - p.ntx;
+                        if (__ldcg(Sp + Tn) == want) dil |= __ldcg(Dp + Tn * TROWS + row + TY - 1);
+                    }
+                    if (yl + 1 < TY) {
+                        if (own) dil |= __ldcg(Dp + base + row + 1);
+                    } else if (ty + 1 < p.nty) {
+                        const uint32_t Tn = T + p.ntx;
+                        if (__ldcg(Sp + Tn) == want) dil |= __ldcg(Dp + Tn * TROWS + row - (TY - 1));
+                    }
+                    if (DIM == 3) {
+                        const uint32_t pl = p.ntx * p.nty;
+                        if (zl > 0) {
+                            if (own) dil |= __ldcg(Dp + base + row - TY);
+                        } else if (tz > 0) {
+                            const uint32_t Tn = T - pl;
+                            if (__ldcg(Sp + Tn) == want) dil |= __ldcg(Dp + Tn * TROWS + row + (TZ - 1) * TY);
+                        }
+                        if (zl + 1 < TZ) {
+                            if (own) dil |= __ldcg(Dp + base + row + TY);
+                        } else if (tz + 1 < p.ntz) {
+                            const uint32_t Tn = T + pl;
+                            if (__ldcg(Sp + Tn) == want) dil |= __ldcg(Dp + Tn * TROWS + row - (TZ - 1) * TY);
+                        }
+                    }
+                    R = c | (dil & ~__ldg(p.TF + base + row));
+                }
+                sR[row] = R;
+                sD[row] = 0;
+                // (3a) compaction offsets: scan of popc over the 64 rows (warps 0 and 1)
+                const unsigned cnt = __popc(R);
+                a_calls += cnt;
+                unsigned inc = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned t = __shfl_up_sync(FULL, inc, o);
+                    if (lane >= (unsigned)o) inc += t;
+                }
+                if (lane == 31) sscan[row >> 5] = inc;
+                soff[row] = inc - cnt;
+            }
+            __syncthreads();
+            if (tid < TROWS) {
+                const uint32_t row = tid;
+                uint32_t b = sR[row];
+                unsigned off = soff[row] + ((row >> 5) ? sscan[0] : 0u);
+                while (b) {
+                    const uint32_t x = __ffs(b) - 1;
+                    b &= b - 1;
+                    mlist[off++] = (uint16_t)((row << 5) | x);
+                }
+            }
+            __syncthreads();
+            const unsigned nm = sscan[0] + sscan[1];
+            // (3) local solves on compacted members
+            for (unsigned i = tid; i < nm; i += BLOCK) {
+                const uint32_t e = mlist[i];
+                const uint32_t x = e & 31u, row = e >> 5, yl = row % TY, zl = row / TY;
+                const unsigned h = ((DIM == 3 ? (zl + 1) * HY : 0u) + (yl + 1)) * HX + (x + 1);
+                Sten s;
+                s.c = halo[h];
+                s.w = halo[h - 1];
+                s.e = halo[h + 1];
+                s.s = halo[h - HX];
+                s.n = halo[h + HX];
+                if (DIM == 3) {
+                    s.d = halo[h - HZS];
+                    s.u = halo[h + HZS];
+                } else {
+                    s.d = s.u = INFINITY;
+                }
+                const uint32_t c = ((z0 + zl) * ny + (y0 + yl)) * nx + (x0 + x);
+                s.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
+                const double v = solve<DIM, SOL>(p, s);
+                const bool dec = v < s.c - p.tol;  // E/ifim.py:203
+                Pn[c] = dec ? v : s.c;
+                if (dec) atomicOr(&sD[row], 1u << x);
+            }
+            __syncthreads();
+            // (4) publish D_r(brick) and push next-round candidates
+            if (nm > 0 && tid < TROWS) {
+                const uint32_t row = tid, yl = row % TY, zl = row / TY;
+                const uint32_t d = sD[row];
+                Dc[T * TROWS + row] = d;
+                a_dec += __popc(d);
+                unsigned f = 0;
+                if (d) f |= 1u;
+                if (d & 1u) f |= 2u;
+                if (d & 0x80000000u) f |= 4u;
+                if (yl == 0 && d) f |= 8u;
+                if (yl == TY - 1 && d) f |= 16u;
+                if (DIM == 3 && zl == 0 && d) f |= 32u;
+                if (DIM == 3 && zl == TZ - 1 && d) f |= 64u;
+                if (f) atomicOr(&s_flags, f);
+            }
+            __syncthreads();
+            if (nm > 0 && tid < 8) {
+                const unsigned f = s_flags;
+                if (tid == 0) Sc[T] = r;
+                const uint32_t nxt = r + 1;
+                const uint32_t pl = p.ntx * p.nty;
+                if (tid == 0 && (f & 1u)) push_brick(p, T, nxt, TLn, lenN);
+                if (tid == 1 && (f & 2u) && tx > 0) push_brick(p, T - 1, nxt, TLn, lenN);
+                if (tid == 2 && (f & 4u) && tx + 1 < p.ntx) push_brick(p, T + 1, nxt, TLn, lenN);
+                if (tid == 3 && (f & 8u) && ty > 0) push_brick(p, T - p.ntx, nxt, TLn, lenN);
+                if (tid == 4 && (f & 16u) && ty + 1 < p.nty) push_brick(p, T + p.ntx, nxt, TLn, lenN);
+                if (DIM == 3 && tid == 5 && (f & 32u) && tz > 0) push_brick(p, T - pl, nxt, TLn, lenN);
+                if (DIM == 3 && tid == 6 && (f & 64u) && tz + 1 < p.ntz) push_brick(p, T + pl, nxt, TLn, lenN);
+            }
+            __syncthreads();
+            if (tid == 0) s_flags = 0;
+        }
+        const unsigned long long tc = block_sum(a_calls, sred);
+        const unsigned long long td = block_sum(a_dec, sred);
+        if (tid == 0) {
+            if (tc) atomicAdd(&ctl->cnt[r % 3], tc);
+            if (td) atomicAdd(&ctl->dsum[r % 3], td);
             if (blockIdx.x == 0) {
+                // len[(r+2)%3] was last read at the start of round r-1; cnt/dsum
+                // slot (r+1)%3 was last read after round r-2's barrier.  Slot r%3
+                // must stay intact until every CTA has read it after this barrier.
                 ctl->len[(r + 2) % 3] = 0;
-                ctl->cnt[(r + 2) % 3] = 0;
+                ctl->cnt[(r + 1) % 3] = 0;
+                ctl->dsum[(r + 1) % 3] = 0;
             }
         }
-        grid_barrier(ctl);
-        const unsigned long long m = vload(&ctl->cnt[(r + 1) % 3]);
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (!grid_barrier(ctl)) return;
+        const unsigned long long calls = vload(&ctl->cnt[r % 3]);
+        const unsigned long long decs = vload(&ctl->dsum[r % 3]);
+        if (blockIdx.x == 0 && tid == 0) {
             ctl->iters = r + 1;
-            ctl->sum += vload(&ctl->cnt[r % 3]);
-            if (m > ctl->peak) ctl->peak = m;
+            ctl->sum += calls;
+            if (calls > ctl->peak) ctl->peak = calls;
+            ctl->writes += decs;
         }
-        if (m == 0) break;
-        if (r + 1 >= p.cap) {  // E/ifim.py:185-189
-            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
+        if (decs == 0) break;
+        if (r + 1 >= (uint32_t)p.cap) {  // E/ifim.py:185-189
+            if (blockIdx.x == 0 && tid == 0) ctl->err = EIK_ECAP;
             break;
         }
     }
-    const unsigned long long td = block_sum(a_dec, sred);
-    if (threadIdx.x == 0) atomicAdd(&ctl->writes, td);
 }
 
 // Element-wise local solver (parity hook).
@@ -855,13 +965,6 @@ __global__ void k_local(int kind, const double *a, const double *b, const double
         else if (kind == 1) out[i] = upd2a(a[i], b[i], f[i], dx, dy);
         else out[i] = upd3u(a[i], b[i], c[i], dx / f[i], dx);
     }
-}
-
-// Copy P1 into P0 (used only on the error path to expose the latest field).
-__global__ void k_copy(double *dst, const double *src, int64_t n)
-{
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        dst[i] = src[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -881,9 +984,9 @@ int fail(int code, const char *fmt, ...)
     return code;
 }
 
-#define CK(call)                                                                              \
-    do {                                                                                      \
-        cudaError_t e_ = (call);                                                              \
+#define CK(call)                                                                                \
+    do {                                                                                        \
+        cudaError_t e_ = (call);                                                                \
         if (e_ != cudaSuccess) return fail(EIK_ECUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
     } while (0)
 
@@ -892,7 +995,10 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
     int64_t N;
     uint32_t W, nwords;
-    size_t off_phi2, off_dd, off_b0, off_b1, off_bt, off_bf, off_l0, off_l1, off_hist, off_ctl_u, off_ctl_r, total;
+    uint32_t ntx, nty, ntz, ntiles;
+    size_t off_phi2, off_dd, off_bt, off_l0, off_l1;
+    size_t off_tr0, off_td0, off_td1, off_tf, off_ts0, off_ts1, off_tc, off_tl0, off_tl1;
+    size_t off_hist, off_ctl_u, off_ctl_r, total;
     int64_t cap_upd, cap_rem;
 };
 
@@ -907,24 +1013,37 @@ int make_layout(const eik_geom *g, Layout &L)
         return fail(EIK_EINVAL, "3D grids require dx == dy == dz (no anisotropic 3D solver, SPEC.md:169)");
     if (g->dtype != EIK_F64) return fail(EIK_EINVAL, "only float64 is supported");
     L.N = g->nx * g->ny * g->nz;
+    if (L.N >= (int64_t)1 << 31)
+        return fail(EIK_EINVAL, "grid too large: %lld cells (limit 2^31 per device)", (long long)L.N);
     const int64_t W = (g->nx + 31) / 32;
     const int64_t nw = W * g->ny * g->nz;
-    if (L.N >= (int64_t)1 << 31) return fail(EIK_EINVAL, "grid too large: %lld cells (limit 2^31 per device)", (long long)L.N);
     L.W = (uint32_t)W;
     L.nwords = (uint32_t)nw;
+    const int TY = g->ndim == 3 ? Brick<3>::TY : Brick<2>::TY;
+    const int TZ = g->ndim == 3 ? Brick<3>::TZ : Brick<2>::TZ;
+    L.ntx = (uint32_t)W;
+    L.nty = (uint32_t)((g->ny + TY - 1) / TY);
+    L.ntz = (uint32_t)((g->nz + TZ - 1) / TZ);
+    L.ntiles = L.ntx * L.nty * L.ntz;
     const int64_t s = g->nx + g->ny + (g->ndim == 3 ? g->nz : 0);
     L.cap_upd = 40 * s;  // E/ifim.py:106 (2D: 40*(nx+ny))
     L.cap_rem = 20 * s;  // E/ifim.py:185
+    const size_t tb = (size_t)L.ntiles * TROWS * 4, ti = (size_t)L.ntiles * 4;
     size_t o = 0;
     L.off_phi2 = o; o += al((size_t)L.N * 8);
     L.off_dd = o; o += al((size_t)L.N * 8);
-    L.off_b0 = o; o += al((size_t)nw * 4);
-    L.off_b1 = o; o += al((size_t)nw * 4);
     L.off_bt = o; o += al((size_t)nw * 4);
-    L.off_bf = o; o += al((size_t)nw * 4);
-    const size_t lst = std::max((size_t)L.N * 4, (size_t)nw * 8);  // cell list or (word, bits) list
-    L.off_l0 = o; o += al(lst);
-    L.off_l1 = o; o += al(lst);
+    L.off_l0 = o; o += al((size_t)L.N * 4);
+    L.off_l1 = o; o += al((size_t)L.N * 4);
+    L.off_tr0 = o; o += al(tb);
+    L.off_td0 = o; o += al(tb);
+    L.off_td1 = o; o += al(tb);
+    L.off_tf = o; o += al(tb);
+    L.off_ts0 = o; o += al(ti);
+    L.off_ts1 = o; o += al(ti);
+    L.off_tc = o; o += al(ti);
+    L.off_tl0 = o; o += al(ti);
+    L.off_tl1 = o; o += al(ti);
     L.off_hist = o; o += al((size_t)(L.cap_upd + 2) * 8);
     L.off_ctl_u = o; o += al(sizeof(Ctl));
     L.off_ctl_r = o; o += al(sizeof(Ctl));
@@ -946,6 +1065,8 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const doub
     memset(&p, 0, sizeof(p));
     p.nx = g->nx; p.ny = g->ny; p.nz = g->nz; p.plane = g->nx * g->ny;
     p.W = L.W; p.nwords = L.nwords; p.nrows = (uint32_t)(g->ny * g->nz);
+    p.nx32 = (uint32_t)g->nx;
+    p.plane32 = (uint32_t)(g->nx * g->ny);
     p.fnx = make_fastdiv((uint32_t)g->nx);
     p.fny = make_fastdiv((uint32_t)g->ny);
     p.fW = make_fastdiv(L.W);
@@ -955,16 +1076,25 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const doub
     p.F = speed;
     p.dd = (double *)(b + L.off_dd);
     p.state = state;
-    p.B0 = (uint32_t *)(b + L.off_b0);
-    p.B1 = (uint32_t *)(b + L.off_b1);
     p.Bt = (uint32_t *)(b + L.off_bt);
-    p.Bf = (uint32_t *)(b + L.off_bf);
     p.L0 = (uint32_t *)(b + L.off_l0);
     p.L1 = (uint32_t *)(b + L.off_l1);
     p.ctl = ctl;
     p.hist = (int64_t *)(b + L.off_hist);
     p.hist_cap = L.cap_upd + 2;
     p.cap = cap;
+    p.ntx = L.ntx; p.nty = L.nty; p.ntz = L.ntz; p.ntiles = L.ntiles;
+    p.fntx = make_fastdiv(L.ntx);
+    p.fnty = make_fastdiv(L.nty);
+    p.TR0 = (uint32_t *)(b + L.off_tr0);
+    p.TD0 = (uint32_t *)(b + L.off_td0);
+    p.TD1 = (uint32_t *)(b + L.off_td1);
+    p.TF = (uint32_t *)(b + L.off_tf);
+    p.TS0 = (uint32_t *)(b + L.off_ts0);
+    p.TS1 = (uint32_t *)(b + L.off_ts1);
+    p.TC = (uint32_t *)(b + L.off_tc);
+    p.TL0 = (uint32_t *)(b + L.off_tl0);
+    p.TL1 = (uint32_t *)(b + L.off_tl1);
     return p;
 }
 
@@ -1011,11 +1141,13 @@ int coop_launch(K kernel, KP &p, const unsigned *skip, bool with_skip, cudaStrea
 
 template <int DIM, int SOL>
 struct Engine {
-    static int prep(KP &p, bool copy_phi, bool touched, uint32_t *c0, uint32_t *c1, cudaStream_t st)
+    // phi copy (optional), d = delta/F, touched (optional) and the fixed brick bitmap
+    static int prep(KP &p, bool copy_phi, bool touched, cudaStream_t st)
     {
+        CK(cudaMemsetAsync(p.TF, 0xff, (size_t)p.ntiles * TROWS * 4, st));
         const int grid = stream_grid(p.nwords);
-        if (SOL == SOL_A2) k_prep<false><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched, c0, c1);
-        else k_prep<true><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched, c0, c1);
+        if (SOL == SOL_A2) k_prep<DIM, false><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched);
+        else k_prep<DIM, true><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched);
         CK(cudaGetLastError());
         return EIK_OK;
     }
@@ -1027,15 +1159,40 @@ struct Engine {
         return EIK_OK;
     }
     static int update(KP &p, cudaStream_t st) { return coop_launch(k_update<DIM, SOL>, p, nullptr, false, st); }
+    // remedy-set slots: R0 bitmap, brick list 0, candidate stamps, counters
+    static int reset_set(KP &p, cudaStream_t st)
+    {
+        CK(cudaMemsetAsync(p.ctl, 0, sizeof(Ctl), st));
+        CK(cudaMemsetAsync(p.TR0, 0, (size_t)p.ntiles * TROWS * 4, st));
+        CK(cudaMemsetAsync(p.TC, 0xff, (size_t)p.ntiles * 4, st));
+        return EIK_OK;
+    }
     static int build(KP &p, const double *Pc, const unsigned *skip, cudaStream_t st)
     {
-        const int grid = stream_grid(p.nwords);
-        k_build<DIM, SOL><<<grid, BLOCK, 0, st>>>(p, Pc, reinterpret_cast<uint2 *>(p.L0), p.B0, skip);
+        int rc = reset_set(p, st);
+        if (rc) return rc;
+        k_build<DIM, SOL><<<stream_grid(p.nwords), BLOCK, 0, st>>>(p, Pc, skip);
+        CK(cudaGetLastError());
+        return EIK_OK;
+    }
+    static int load(KP &p, const uint8_t *member, cudaStream_t st)
+    {
+        int rc = reset_set(p, st);
+        if (rc) return rc;
+        k_remedy_load<DIM><<<stream_grid(p.nwords), BLOCK, 0, st>>>(p, member);
+        CK(cudaGetLastError());
+        return EIK_OK;
+    }
+    static int do_export(KP &p, unsigned n, uint8_t *member, cudaStream_t st)
+    {
+        if (n) k_remedy_export<DIM><<<(int)std::min<unsigned>(n, 4096u), BLOCK, 0, st>>>(p, n, member);
         CK(cudaGetLastError());
         return EIK_OK;
     }
     static int remedy(KP &p, const unsigned *skip, cudaStream_t st)
     {
+        CK(cudaMemsetAsync(p.TS0, 0xff, (size_t)p.ntiles * 4, st));
+        CK(cudaMemsetAsync(p.TS1, 0xff, (size_t)p.ntiles * 4, st));
         return coop_launch(k_remedy<DIM, SOL>, p, skip, true, st);
     }
 };
@@ -1052,7 +1209,6 @@ int dispatch(const eik_geom *g, F &&f)
 
 struct Events {
     cudaEvent_t e[8];
-    int n = 0;
     Events() { for (auto &x : e) cudaEventCreate(&x); }
     ~Events() { for (auto &x : e) cudaEventDestroy(x); }
     void rec(int i, cudaStream_t s) { cudaEventRecord(e[i], s); }
@@ -1072,8 +1228,6 @@ int check_ws(const Layout &L, void *ws, size_t bytes)
     return EIK_OK;
 }
 
-// Phases shared by solve and the staged entry points --------------------------------
-
 int run_update(const eik_geom *g, const Layout &L, double *phi, const double *speed, uint8_t *state,
                const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol, void *ws,
                cudaStream_t st, int64_t &launches)
@@ -1089,7 +1243,7 @@ int run_update(const eik_geom *g, const Layout &L, double *phi, const double *sp
     }
     KP p = make_kp(g, L, ws, phi, speed, state, tol, ctl, L.cap_upd);
     return dispatch(g, [&](auto E) {
-        int rc = E.prep(p, true, true, p.B0, p.B1, st);
+        int rc = E.prep(p, true, true, st);
         if (rc) return rc;
         rc = E.init_active(p, seed_idx, nseeds, st);
         if (rc) return rc;
@@ -1099,6 +1253,14 @@ int run_update(const eik_geom *g, const Layout &L, double *phi, const double *sp
     });
 }
 
+int check_hang(const Ctl &c, const char *what)
+{
+    if (c.err == EIK_EHANG)
+        return fail(EIK_ECUDA, "%s: device watchdog fired at iteration %llu (grid barrier timeout)", what,
+                    (unsigned long long)c.iters);
+    return EIK_OK;
+}
+
 void fill_update_stats(const Ctl &c, eik_stats *o)
 {
     o->upd_iterations = (int64_t)c.iters;
@@ -1106,6 +1268,15 @@ void fill_update_stats(const Ctl &c, eik_stats *o)
     o->peak_active = (int64_t)c.peak;
     o->converged = (int64_t)c.conv;
     o->history_len = (int64_t)c.iters;
+}
+
+int expose_latest(const Layout &L, const Ctl &c, double *phi, const double *phi2, cudaStream_t st)
+{
+    if (c.iters & 1) {  // the newest values sit in the workspace buffer
+        CK(cudaMemcpyAsync(phi, phi2, (size_t)L.N * 8, cudaMemcpyDeviceToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    return EIK_OK;
 }
 
 }  // namespace
@@ -1118,7 +1289,10 @@ extern "C" {
 
 const char *eik_last_error(void) { return g_err.c_str(); }
 
-const char *eik_version(void) { return "eik_ifim 0.1 (sm_100a, float64 bit-exact, persistent grid-barrier engine)"; }
+const char *eik_version(void)
+{
+    return "eik_ifim 0.2 (sm_100a, float64 bit-exact; persistent update worklist + brick-staged remedy)";
+}
 
 int eik_workspace_size(const eik_geom *g, size_t *bytes)
 {
@@ -1154,10 +1328,7 @@ int eik_ifim_update_step(const eik_geom *g, double *phi, const double *speed, ui
     char *b = (char *)workspace;
     CK(cudaMemcpyAsync(&c, b + L.off_ctl_u, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (c.err == EIK_ECAP && (c.iters & 1)) {  // expose the latest buffer like the reference would
-        k_copy<<<1024, 256, 0, st>>>(phi, (const double *)(b + L.off_phi2), L.N);
-        CK(cudaStreamSynchronize(st));
-    }
+    if ((rc = check_hang(c, "update step"))) return rc;
     fill_update_stats(c, out);
     out->iterations = out->upd_iterations;
     out->solver_calls = out->upd_calls;
@@ -1168,8 +1339,10 @@ int eik_ifim_update_step(const eik_geom *g, double *phi, const double *speed, ui
         const int64_t n = std::min<int64_t>((int64_t)c.iters, history_cap);
         CK(cudaMemcpy(history, b + L.off_hist, (size_t)n * 8, cudaMemcpyDeviceToHost));
     }
-    if (c.err == EIK_ECAP)
+    if (c.err == EIK_ECAP) {
+        if ((rc = expose_latest(L, c, phi, (const double *)(b + L.off_phi2), st))) return rc;
         return fail(EIK_ECAP, "active list did not drain within %lld iterations", (long long)L.cap_upd);
+    }
     return EIK_OK;
 }
 
@@ -1188,10 +1361,9 @@ int eik_build_remedy(const eik_geom *g, const double *phi, const double *speed, 
     Ctl *ctl = (Ctl *)(b + L.off_ctl_r);
     Events ev;
     ev.rec(0, st);
-    CK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
     KP p = make_kp(g, L, workspace, const_cast<double *>(phi), speed, state, tol, ctl, L.cap_rem);
     rc = dispatch(g, [&](auto E) {
-        int r = E.prep(p, false, false, nullptr, nullptr, st);
+        int r = E.prep(p, false, false, st);
         if (r) return r;
         return E.build(p, phi, nullptr, st);
     });
@@ -1218,14 +1390,13 @@ int eik_remedy_load(const eik_geom *g, const uint8_t *member, const uint8_t *sta
     cudaStream_t st = (cudaStream_t)stream;
     char *b = (char *)workspace;
     Ctl *ctl = (Ctl *)(b + L.off_ctl_r);
-    CK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
     KP p = make_kp(g, L, workspace, nullptr, nullptr, state, 1e-12, ctl, L.cap_rem);
-    k_remedy_load<<<stream_grid(p.nwords), BLOCK, 0, st>>>(p, member, reinterpret_cast<uint2 *>(p.L0), p.B0);
-    CK(cudaGetLastError());
+    rc = dispatch(g, [&](auto E) { return E.load(p, member, st); });
+    if (rc) return rc;
     Ctl c;
     CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (count) *count = (int64_t)c.cnt[0];
+    if (count) *count = (int64_t)c.flagged;
     return EIK_OK;
 }
 
@@ -1243,11 +1414,8 @@ int eik_remedy_export(const eik_geom *g, void *workspace, size_t workspace_bytes
     CK(cudaStreamSynchronize(st));
     CK(cudaMemsetAsync(member, 0, (size_t)L.N, st));
     KP p = make_kp(g, L, workspace, nullptr, nullptr, nullptr, 1e-12, nullptr, 0);
-    if (c.len[0]) {
-        k_remedy_export<<<stream_grid(c.len[0]), BLOCK, 0, st>>>(p, reinterpret_cast<const uint2 *>(p.L0), c.len[0],
-                                                                 member);
-        CK(cudaGetLastError());
-    }
+    rc = dispatch(g, [&](auto E) { return E.do_export(p, c.len[0], member, st); });
+    if (rc) return rc;
     CK(cudaStreamSynchronize(st));
     return EIK_OK;
 }
@@ -1270,7 +1438,7 @@ int eik_remedy_step(const eik_geom *g, double *phi, const double *speed, const u
     KP p = make_kp(g, L, workspace, phi, speed, state, tol, ctl, L.cap_rem);
     // staged call: the caller may have edited phi since the last call
     rc = dispatch(g, [&](auto E) {
-        int r = E.prep(p, true, false, nullptr, nullptr, st);
+        int r = E.prep(p, true, false, st);
         if (r) return r;
         return E.remedy(p, nullptr, st);
     });
@@ -1279,17 +1447,17 @@ int eik_remedy_step(const eik_geom *g, double *phi, const double *speed, const u
     Ctl c;
     CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (c.err == EIK_ECAP && (c.iters & 1)) {
-        k_copy<<<1024, 256, 0, st>>>(phi, p.P1, L.N);
-        CK(cudaStreamSynchronize(st));
-    }
+    if ((rc = check_hang(c, "remedy step"))) return rc;
     out->rem_iterations = out->iterations = (int64_t)c.iters;
     out->rem_calls = out->solver_calls = (int64_t)c.sum;
     out->peak_remedy = (int64_t)c.peak;
     out->phi_writes = (int64_t)c.writes;
     out->gpu_launches = 2;
     out->rem_ms = out->total_ms = ev.ms(0, 1);
-    if (c.err == EIK_ECAP) return fail(EIK_ECAP, "remedy set did not drain within %lld rounds", (long long)L.cap_rem);
+    if (c.err == EIK_ECAP) {
+        if ((rc = expose_latest(L, c, phi, p.P1, st))) return rc;
+        return fail(EIK_ECAP, "remedy set did not drain within %lld rounds", (long long)L.cap_rem);
+    }
     return EIK_OK;
 }
 
@@ -1315,7 +1483,6 @@ int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t 
     rc = run_update(g, L, phi, speed, state, seed_idx, seed_val, nseeds, tol, workspace, st, launches);
     if (rc) return rc;
     ev.rec(1, st);
-    CK(cudaMemsetAsync(cr, 0, sizeof(Ctl), st));
     KP p = make_kp(g, L, workspace, phi, speed, state, tol, cr, L.cap_rem);
     // After a drained update step both phi buffers are identical (every cell
     // changed in the last-but-one iteration rewrote itself in the last one),
@@ -1332,18 +1499,13 @@ int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t 
     CK(cudaMemcpyAsync(&c[0], cu, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&c[1], cr, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if ((rc = check_hang(c[0], "update step")) || (rc = check_hang(c[1], "remedy step"))) return rc;
     if (c[0].err == EIK_ECAP) {
-        if (c[0].iters & 1) {
-            k_copy<<<1024, 256, 0, st>>>(phi, p.P1, L.N);
-            CK(cudaStreamSynchronize(st));
-        }
+        if ((rc = expose_latest(L, c[0], phi, p.P1, st))) return rc;
         return fail(EIK_ECAP, "active list did not drain within %lld iterations", (long long)L.cap_upd);
     }
     if (c[1].err == EIK_ECAP) {
-        if (c[1].iters & 1) {
-            k_copy<<<1024, 256, 0, st>>>(phi, p.P1, L.N);
-            CK(cudaStreamSynchronize(st));
-        }
+        if ((rc = expose_latest(L, c[1], phi, p.P1, st))) return rc;
         return fail(EIK_ECAP, "remedy set did not drain within %lld rounds", (long long)L.cap_rem);
     }
     fill_update_stats(c[0], out);
