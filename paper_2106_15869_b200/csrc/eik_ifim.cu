@@ -110,33 +110,12 @@ struct KP {
     int64_t *hist;
     int64_t hist_cap;
     int64_t cap;
-    // remedy bricks: 32 x TY x TZ cells, 64 row words per brick (tile-major bitmaps)
-    uint32_t ntx, nty, ntz, ntiles;
-    FastDiv fntx, fnty;
-    uint32_t *TR0, *TD0, *TD1, *TF;     // R0, D (double-buffered), fixed
-    uint32_t *TS0, *TS1, *TC;          // D round stamps (per parity), candidate stamps
-    uint32_t *TL0, *TL1;               // brick worklists
+    // remedy step: row-major bitmaps (one word per 32 cells of an x-row)
+    uint32_t *R0b;       // R_0 (build / load)
+    uint32_t *D0b, *D1b;  // D_r (decreased cells), double-buffered by round parity
+    uint32_t *Fb;        // fixed = blocked | source | outside the row
 };
 
-template <int DIM>
-struct Brick;
-template <>
-struct Brick<3> {
-    static constexpr int TY = 8, TZ = 8;
-};
-template <>
-struct Brick<2> {
-    static constexpr int TY = 64, TZ = 1;
-};
-constexpr int TROWS = 64;  // TY * TZ row words per brick
-
-template <int DIM>
-__device__ __forceinline__ uint32_t brick_row_index(const KP &p, uint32_t wx, uint32_t y, uint32_t z)
-{
-    constexpr int TY = Brick<DIM>::TY, TZ = Brick<DIM>::TZ;
-    const uint32_t T = ((z / TZ) * p.nty + y / TY) * p.ntx + wx;
-    return T * TROWS + (z % TZ) * TY + (y % TY);
-}
 
 
 // ---------------------------------------------------------------------------
@@ -465,7 +444,7 @@ __global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_
         const uint32_t blk = __ballot_sync(FULL, in && st == ST_BLOCKED);
         const uint32_t src = __ballot_sync(FULL, in && st == ST_SOURCE);
         if (lane == 0) {
-            p.TF[brick_row_index<DIM>(p, q.wx, q.y, q.z)] = blk | src | ~q.rowm;  // out-of-grid lanes are fixed
+            p.Fb[w] = blk | src | ~q.rowm;  // lanes outside the row count as fixed
             if (build_touched) p.Bt[w] = blk;
         }
     }
@@ -554,15 +533,15 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
                     y = r;
                 }
                 Sten s;
-                s.c = ldcg(Pc + c);
-                s.w = x > 0 ? ldcg(Pc + (c - 1)) : INFINITY;
-                s.e = x + 1 < nx ? ldcg(Pc + (c + 1)) : INFINITY;
-                s.s = y > 0 ? ldcg(Pc + (c - nx)) : INFINITY;
-                s.n = y + 1 < ny ? ldcg(Pc + (c + nx)) : INFINITY;
+                s.c = __ldca(Pc + c);
+                s.w = x > 0 ? __ldca(Pc + (c - 1)) : INFINITY;
+                s.e = x + 1 < nx ? __ldca(Pc + (c + 1)) : INFINITY;
+                s.s = y > 0 ? __ldca(Pc + (c - nx)) : INFINITY;
+                s.n = y + 1 < ny ? __ldca(Pc + (c + nx)) : INFINITY;
                 s.d = s.u = INFINITY;
                 if (DIM == 3) {
-                    s.d = z > 0 ? ldcg(Pc + (c - p.plane32)) : INFINITY;
-                    s.u = z + 1 < nz ? ldcg(Pc + (c + p.plane32)) : INFINITY;
+                    s.d = z > 0 ? __ldca(Pc + (c - p.plane32)) : INFINITY;
+                    s.u = z + 1 < nz ? __ldca(Pc + (c + p.plane32)) : INFINITY;
                 }
                 s.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
                 const double v = solve<DIM, SOL>(p, s);
@@ -631,19 +610,8 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
 }
 
 // ---------------------------------------------------------------------------
-// Brick helpers.  Brick T = (tz * nty + ty) * ntx + tx covers x in
-// [32 tx, 32 tx + 32), y in [TY ty, ...), z in [TZ tz, ...); its 64 row words
-// live at T * 64 + (z % TZ) * TY + (y % TY) in every tile-major bitmap.
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ void push_brick(const KP &p, uint32_t T, uint32_t stamp, uint32_t *list, unsigned *len)
-{
-    if (atomicExch(p.TC + T, stamp) != stamp) list[atomicAdd(len, 1u)] = T;
-}
-
-// ---------------------------------------------------------------------------
 // Build pass (E/ifim.py:137-161): one value per free cell, flag |v - phi| > tol.
-// Writes R0 into the tile-major bitmap and the list of bricks holding it.
+// Writes R_0 as a row-major bitmap (every word) and counts it.
 // ---------------------------------------------------------------------------
 
 template <int DIM, int SOL>
@@ -658,24 +626,22 @@ __global__ void __launch_bounds__(BLOCK) k_build(KP p, const double *__restrict_
     unsigned long long a_free = 0, a_flag = 0;
     for (uint32_t w = gw; w < p.nwords; w += GW) {
         const WPos q = wpos<DIM>(p, w);
-        const uint32_t ri = brick_row_index<DIM>(p, q.wx, q.y, q.z);
-        const uint32_t freem = q.rowm & ~__ldg(p.TF + ri);
-        if (freem == 0) continue;
-        Sten s;
-        gather<DIM, SOL>(p, Pc, q, freem, s);
-        bool moved = false;
-        if ((freem >> lane) & 1u) {
-            const double v = solve<DIM, SOL>(p, s);
-            moved = fabs(v - s.c) > p.tol;  // NaN (inf - inf) is not flagged
-        }
-        const uint32_t mm = __ballot_sync(FULL, moved);
-        if (lane == 0) {
-            a_free += __popc(freem);
-            if (mm) {
-                a_flag += __popc(mm);
-                p.TR0[ri] = mm;
-                push_brick(p, ri / TROWS, 0u, p.TL0, &ctl->len[0]);
+        const uint32_t freem = q.rowm & ~__ldg(p.Fb + w);
+        uint32_t mm = 0;
+        if (freem) {
+            Sten s;
+            gather<DIM, SOL>(p, Pc, q, freem, s);
+            bool moved = false;
+            if ((freem >> lane) & 1u) {
+                const double v = solve<DIM, SOL>(p, s);
+                moved = fabs(v - s.c) > p.tol;  // NaN (inf - inf) is not flagged
             }
+            mm = __ballot_sync(FULL, moved);
+        }
+        if (lane == 0) {
+            p.R0b[w] = mm;
+            a_free += __popc(freem);
+            a_flag += __popc(mm);
         }
     }
     const unsigned long long tf = block_sum(a_free, sred);
@@ -698,10 +664,8 @@ __global__ void __launch_bounds__(BLOCK) k_remedy_load(KP p, const uint8_t *memb
         const WPos q = wpos<DIM>(p, w);
         const bool in = (q.rowm >> lane) & 1u;
         const uint32_t m = __ballot_sync(FULL, in && member[q.c0 + lane] != 0);
-        if (lane == 0 && m) {
-            const uint32_t ri = brick_row_index<DIM>(p, q.wx, q.y, q.z);
-            p.TR0[ri] = m;
-            push_brick(p, ri / TROWS, 0u, p.TL0, &p.ctl->len[0]);
+        if (lane == 0) {
+            p.R0b[w] = m;
             cnt += __popc(m);
         }
     }
@@ -709,248 +673,188 @@ __global__ void __launch_bounds__(BLOCK) k_remedy_load(KP p, const uint8_t *memb
 }
 
 template <int DIM>
-__global__ void k_remedy_export(KP p, unsigned n, uint8_t *member)
+__global__ void k_remedy_export(KP p, uint8_t *member)
 {
-    constexpr int TY = Brick<DIM>::TY;
-    for (uint32_t i = blockIdx.x; i < n; i += gridDim.x) {
-        const uint32_t T = p.TL0[i];
-        const uint32_t t1 = fdiv(T, p.fntx), tx = T - t1 * p.ntx;
-        const uint32_t tz = fdiv(t1, p.fnty), ty = t1 - tz * p.nty;
-        for (uint32_t e = threadIdx.x; e < TROWS * 32; e += blockDim.x) {
-            const uint32_t row = e >> 5, x = e & 31;
-            if ((p.TR0[T * TROWS + row] >> x) & 1u) {
-                const uint32_t gx = tx * 32 + x, gy = ty * TY + row % TY, gz = tz * Brick<DIM>::TZ + row / TY;
-                member[(gz * (uint32_t)p.ny + gy) * p.nx32 + gx] = 1;
+    const unsigned lane = lane_id();
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t w = gw; w < p.nwords; w += GW) {
+        const uint32_t m = p.R0b[w];
+        if (m == 0) continue;
+        const WPos q = wpos<DIM>(p, w);
+        if ((m >> lane) & 1u) member[q.c0 + lane] = 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Remedy step (E/ifim.py:164-218): persistent kernel, two grid barriers per
+// round.
+//   B: R_r = R_0 (round 0) or D_{r-1} | (N(D_{r-1}) & ~fixed) (E/ifim.py:209-214
+//      in set form: membership only deduplicates), one thread per bitmap word;
+//      the members are compacted, in word order, into a cell list.
+//   A: one thread per member: v from the snapshot; v < phi - tol writes P_next
+//      and sets the member's D_r bit, otherwise the member drops
+//      (E/ifim.py:199-208).
+// |R_r| is the list length, |D_r| a counter; the loop ends when D_r is empty.
+// ---------------------------------------------------------------------------
+
+constexpr int REM_PER = 4;  // bitmap words per thread in phase B
+
+template <int DIM>
+__device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint32_t *__restrict__ Dp,
+                                            uint32_t *Dc, uint32_t *ML, unsigned *lenR, unsigned *sscan)
+{
+    const uint32_t chunk = BLOCK * REM_PER;
+    const uint32_t planeW = (uint32_t)p.ny * p.W;
+    for (uint32_t base = blockIdx.x * chunk; base < p.nwords; base += gridDim.x * chunk) {
+        uint32_t R[REM_PER];
+        unsigned cnt = 0;
+#pragma unroll
+        for (int k = 0; k < REM_PER; ++k) {
+            const uint32_t w = base + threadIdx.x + k * BLOCK;
+            R[k] = 0;
+            if (w < p.nwords) {
+                if (r == 0) {
+                    R[k] = __ldcg(p.R0b + w);
+                } else {
+                    const uint32_t row = fdiv(w, p.fW);
+                    const uint32_t wx = w - row * p.W;
+                    uint32_t y, z;
+                    if (DIM == 3) {
+                        z = fdiv(row, p.fny);
+                        y = row - z * (uint32_t)p.ny;
+                    } else {
+                        z = 0;
+                        y = row;
+                    }
+                    const uint32_t c = __ldcg(Dp + w);
+                    const uint32_t dw = wx > 0 ? __ldcg(Dp + w - 1) : 0u;
+                    const uint32_t de = wx + 1 < p.W ? __ldcg(Dp + w + 1) : 0u;
+                    const uint32_t ds = y > 0 ? __ldcg(Dp + w - p.W) : 0u;
+                    const uint32_t dn = y + 1 < p.ny ? __ldcg(Dp + w + p.W) : 0u;
+                    uint32_t dd = 0, du = 0;
+                    if (DIM == 3) {
+                        dd = z > 0 ? __ldcg(Dp + w - planeW) : 0u;
+                        du = z + 1 < p.nz ? __ldcg(Dp + w + planeW) : 0u;
+                    }
+                    const uint32_t dil = (c << 1) | (c >> 1) | (dw >> 31) | (de << 31) | ds | dn | dd | du;
+                    R[k] = c | (dil & ~__ldg(p.Fb + w));
+                }
+                Dc[w] = 0;  // D_r is accumulated by phase A with atomicOr
+                cnt += __popc(R[k]);
+            }
+        }
+        unsigned pos = block_reserve(cnt, lenR, sscan);
+#pragma unroll
+        for (int k = 0; k < REM_PER; ++k) {
+            uint32_t b = R[k];
+            if (!b) continue;
+            const uint32_t w = base + threadIdx.x + k * BLOCK;
+            const uint32_t row = fdiv(w, p.fW);
+            const uint32_t c0 = row * p.nx32 + (w - row * p.W) * 32u;
+            while (b) {
+                const uint32_t x = __ffs(b) - 1;
+                b &= b - 1;
+                ML[pos++] = c0 + x;
             }
         }
     }
 }
 
-// ---------------------------------------------------------------------------
-// Remedy step (E/ifim.py:164-218): persistent kernel, one grid barrier per
-// round, one brick per CTA at a time.
-//
-// Round r processes the candidate bricks of the round:
-//   1. R_r(brick): round 0 reads R0; later rounds pull
-//      R_r = D_{r-1} | (N(D_{r-1}) & ~fixed) from the brick's own and its six
-//      face neighbours' D_{r-1} words (D words are valid only if the brick's
-//      round stamp says r-1, so no bitmap is ever cleared).
-//   2. phi of the brick plus a one-cell halo is staged in shared memory
-//      (out-of-grid halo = +inf, E/_kernels.py:21-26).
-//   3. Members are compacted so every lane runs a local solve; v < phi - tol
-//      writes P_next and sets the D bit (E/ifim.py:199-208).
-//   4. D_r(brick) is published with its stamp; if non-empty the brick and the
-//      face neighbours its decreases touch become candidates of round r+1
-//      (E/ifim.py:209-213, set form).
-// |R_r| and |D_r| are counted exactly; the loop ends when D_r is empty.
-// ---------------------------------------------------------------------------
-
 template <int DIM, int SOL>
-__global__ void __launch_bounds__(BLOCK, 3) k_remedy(KP p, const unsigned *skip)
+__global__ void __launch_bounds__(BLOCK, 4) k_remedy(KP p, const unsigned *skip)
 {
-    constexpr int TY = Brick<DIM>::TY, TZ = Brick<DIM>::TZ;
-    constexpr int HX = 34, HY = TY + 2, HZ = DIM == 3 ? TZ + 2 : 1;
-    constexpr int HN = HX * HY * HZ;
-    constexpr int HZS = HX * HY;  // halo z stride
-    __shared__ double halo[HN];
-    __shared__ uint32_t sR[TROWS], sD[TROWS];
-    __shared__ uint16_t mlist[TROWS * 32];
-    __shared__ unsigned sscan[2], soff[TROWS];
-    __shared__ unsigned s_flags;
+    __shared__ unsigned sscan[WPB + 1];
     __shared__ unsigned long long sred[WPB];
     if (skip && *skip) return;
     Ctl *ctl = p.ctl;
-    const unsigned tid = threadIdx.x, lane = lane_id();
+    const unsigned lane = lane_id();
     const unsigned long long r0 = vload(&ctl->flagged);
     if (r0 == 0) return;  // empty remedy set: zero rounds
-    if (blockIdx.x == 0 && tid == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctl->peak = r0;
         ctl->sum = 0;
     }
-    if (tid == 0) s_flags = 0;
     const uint32_t nx = p.nx32, ny = (uint32_t)p.ny, nz = (uint32_t)p.nz;
+    const uint32_t gt = blockIdx.x * BLOCK + threadIdx.x, GT = gridDim.x * BLOCK;
+    uint32_t *ML = p.L0;
     for (uint32_t r = 0;; ++r) {
         const int par = (int)(r & 1);
         const double *__restrict__ Pc = par ? p.P1 : p.P0;
         double *__restrict__ Pn = par ? p.P0 : p.P1;
-        uint32_t *Dc = par ? p.TD1 : p.TD0;
-        const uint32_t *Dp = par ? p.TD0 : p.TD1;
-        uint32_t *Sc = par ? p.TS1 : p.TS0;
-        const uint32_t *Sp = par ? p.TS0 : p.TS1;
-        const uint32_t *TLc = par ? p.TL1 : p.TL0;
-        uint32_t *TLn = par ? p.TL0 : p.TL1;
-        unsigned *lenN = &ctl->len[(r + 1) % 3];
-        const unsigned n = vload(&ctl->len[r % 3]);
-        unsigned long long a_calls = 0, a_dec = 0;
-        for (unsigned ti = blockIdx.x; ti < n; ti += gridDim.x) {
-            const uint32_t T = __ldcg(TLc + ti);
-            const uint32_t t1 = fdiv(T, p.fntx), tx = T - t1 * p.ntx;
-            const uint32_t tz = fdiv(t1, p.fnty), ty = t1 - tz * p.nty;
-            const uint32_t x0 = tx * 32, y0 = ty * TY, z0 = tz * TZ;
-            // (2) stage phi + halo
-            for (unsigned i = tid; i < (unsigned)HN; i += BLOCK) {
-                const unsigned hx = i % HX, hy = (i / HX) % HY, hz = i / HZS;
-                const int gx = (int)(x0 + hx) - 1, gy = (int)(y0 + hy) - 1;
-                const int gz = DIM == 3 ? (int)(z0 + hz) - 1 : 0;
-                double v = INFINITY;
-                if (gx >= 0 && gx < (int)nx && gy >= 0 && gy < (int)ny && gz >= 0 && gz < (int)nz)
-                    v = ldcg(Pc + (((uint32_t)gz * ny + (uint32_t)gy) * nx + (uint32_t)gx));
-                halo[i] = v;
-            }
-            // (1) R_r of this brick
-            if (tid < TROWS) {
-                const uint32_t row = tid, yl = row % TY, zl = row / TY;
-                const uint32_t base = T * TROWS;
-                uint32_t R;
-                if (r == 0) {
-                    R = __ldcg(p.TR0 + base + row);
-                } else {
-                    const uint32_t want = r - 1;
-                    const bool own = __ldcg(Sp + T) == want;
-                    const uint32_t c = own ? __ldcg(Dp + base + row) : 0u;
-                    uint32_t dil = (c << 1) | (c >> 1);
-                    if (tx > 0 && __ldcg(Sp + T - 1) == want) dil |= __ldcg(Dp + base - TROWS + row) >> 31;
-                    if (tx + 1 < p.ntx && __ldcg(Sp + T + 1) == want) dil |= __ldcg(Dp + base + TROWS + row) << 31;
-                    if (yl > 0) {
-                        if (own) dil |= __ldcg(Dp + base + row - 1);
-                    } else if (ty > 0) {
-                        const uint32_t Tn = T - p.ntx;
-                        if (__ldcg(Sp + Tn) == want) dil |= __ldcg(Dp + Tn * TROWS + row + TY - 1);
-                    }
-                    if (yl + 1 < TY) {
-                        if (own) dil |= __ldcg(Dp + base + row + 1);
-                    } else if (ty + 1 < p.nty) {
-                        const uint32_t Tn = T + p.ntx;
-                        if (__ldcg(Sp + Tn) == want) dil |= __ldcg(Dp + Tn * TROWS + row - (TY - 1));
-                    }
-                    if (DIM == 3) {
-                        const uint32_t pl = p.ntx * p.nty;
-                        if (zl > 0) {
-                            if (own) dil |= __ldcg(Dp + base + row - TY);
-                        } else if (tz > 0) {
-                            const uint32_t Tn = T - pl;
-                            if (__ldcg(Sp + Tn) == want) dil |= __ldcg(Dp + Tn * TROWS + row + (TZ - 1) * TY);
-                        }
-                        if (zl + 1 < TZ) {
-                            if (own) dil |= __ldcg(Dp + base + row + TY);
-                        } else if (tz + 1 < p.ntz) {
-                            const uint32_t Tn = T + pl;
-                            if (__ldcg(Sp + Tn) == want) dil |= __ldcg(Dp + Tn * TROWS + row - (TZ - 1) * TY);
-                        }
-                    }
-                    R = c | (dil & ~__ldg(p.TF + base + row));
-                }
-                sR[row] = R;
-                sD[row] = 0;
-                // (3a) compaction offsets: scan of popc over the 64 rows (warps 0 and 1)
-                const unsigned cnt = __popc(R);
-                a_calls += cnt;
-                unsigned inc = cnt;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const unsigned t = __shfl_up_sync(FULL, inc, o);
-                    if (lane >= (unsigned)o) inc += t;
-                }
-                if (lane == 31) sscan[row >> 5] = inc;
-                soff[row] = inc - cnt;
-            }
-            __syncthreads();
-            if (tid < TROWS) {
-                const uint32_t row = tid;
-                uint32_t b = sR[row];
-                unsigned off = soff[row] + ((row >> 5) ? sscan[0] : 0u);
-                while (b) {
-                    const uint32_t x = __ffs(b) - 1;
-                    b &= b - 1;
-                    mlist[off++] = (uint16_t)((row << 5) | x);
-                }
-            }
-            __syncthreads();
-            const unsigned nm = sscan[0] + sscan[1];
-            // (3) local solves on compacted members
-            for (unsigned i = tid; i < nm; i += BLOCK) {
-                const uint32_t e = mlist[i];
-                const uint32_t x = e & 31u, row = e >> 5, yl = row % TY, zl = row / TY;
-                const unsigned h = ((DIM == 3 ? (zl + 1) * HY : 0u) + (yl + 1)) * HX + (x + 1);
-                Sten s;
-                s.c = halo[h];
-                s.w = halo[h - 1];
-                s.e = halo[h + 1];
-                s.s = halo[h - HX];
-                s.n = halo[h + HX];
-                if (DIM == 3) {
-                    s.d = halo[h - HZS];
-                    s.u = halo[h + HZS];
-                } else {
-                    s.d = s.u = INFINITY;
-                }
-                const uint32_t c = ((z0 + zl) * ny + (y0 + yl)) * nx + (x0 + x);
-                s.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
-                const double v = solve<DIM, SOL>(p, s);
-                const bool dec = v < s.c - p.tol;  // E/ifim.py:203
-                Pn[c] = dec ? v : s.c;
-                if (dec) atomicOr(&sD[row], 1u << x);
-            }
-            __syncthreads();
-            // (4) publish D_r(brick) and push next-round candidates
-            if (nm > 0 && tid < TROWS) {
-                const uint32_t row = tid, yl = row % TY, zl = row / TY;
-                const uint32_t d = sD[row];
-                Dc[T * TROWS + row] = d;
-                a_dec += __popc(d);
-                unsigned f = 0;
-                if (d) f |= 1u;
-                if (d & 1u) f |= 2u;
-                if (d & 0x80000000u) f |= 4u;
-                if (yl == 0 && d) f |= 8u;
-                if (yl == TY - 1 && d) f |= 16u;
-                if (DIM == 3 && zl == 0 && d) f |= 32u;
-                if (DIM == 3 && zl == TZ - 1 && d) f |= 64u;
-                if (f) atomicOr(&s_flags, f);
-            }
-            __syncthreads();
-            if (nm > 0 && tid < 8) {
-                const unsigned f = s_flags;
-                if (tid == 0) Sc[T] = r;
-                const uint32_t nxt = r + 1;
-                const uint32_t pl = p.ntx * p.nty;
-                if (tid == 0 && (f & 1u)) push_brick(p, T, nxt, TLn, lenN);
-                if (tid == 1 && (f & 2u) && tx > 0) push_brick(p, T - 1, nxt, TLn, lenN);
-                if (tid == 2 && (f & 4u) && tx + 1 < p.ntx) push_brick(p, T + 1, nxt, TLn, lenN);
-                if (tid == 3 && (f & 8u) && ty > 0) push_brick(p, T - p.ntx, nxt, TLn, lenN);
-                if (tid == 4 && (f & 16u) && ty + 1 < p.nty) push_brick(p, T + p.ntx, nxt, TLn, lenN);
-                if (DIM == 3 && tid == 5 && (f & 32u) && tz > 0) push_brick(p, T - pl, nxt, TLn, lenN);
-                if (DIM == 3 && tid == 6 && (f & 64u) && tz + 1 < p.ntz) push_brick(p, T + pl, nxt, TLn, lenN);
-            }
-            __syncthreads();
-            if (tid == 0) s_flags = 0;
-        }
-        const unsigned long long tc = block_sum(a_calls, sred);
-        const unsigned long long td = block_sum(a_dec, sred);
-        if (tid == 0) {
-            if (tc) atomicAdd(&ctl->cnt[r % 3], tc);
-            if (td) atomicAdd(&ctl->dsum[r % 3], td);
-            if (blockIdx.x == 0) {
-                // len[(r+2)%3] was last read at the start of round r-1; cnt/dsum
-                // slot (r+1)%3 was last read after round r-2's barrier.  Slot r%3
-                // must stay intact until every CTA has read it after this barrier.
-                ctl->len[(r + 2) % 3] = 0;
-                ctl->cnt[(r + 1) % 3] = 0;
-                ctl->dsum[(r + 1) % 3] = 0;
-            }
+        uint32_t *Dc = par ? p.D1b : p.D0b;
+        const uint32_t *Dp = par ? p.D0b : p.D1b;
+        unsigned *lenR = &ctl->len[r % 3];
+        // ---- phase B: members of R_r ----
+        rem_members<DIM>(p, r, Dp, Dc, ML, lenR, sscan);
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            // slot (r+1)%3 of len / dsum was last read two rounds ago
+            ctl->len[(r + 1) % 3] = 0;
+            ctl->dsum[(r + 1) % 3] = 0;
         }
         if (!grid_barrier(ctl)) return;
-        const unsigned long long calls = vload(&ctl->cnt[r % 3]);
-        const unsigned long long decs = vload(&ctl->dsum[r % 3]);
-        if (blockIdx.x == 0 && tid == 0) {
+        const unsigned m = vload(lenR);  // |R_r|
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
             ctl->iters = r + 1;
-            ctl->sum += calls;
-            if (calls > ctl->peak) ctl->peak = calls;
-            ctl->writes += decs;
+            ctl->sum += m;
+            if (m > ctl->peak) ctl->peak = m;
         }
+        // ---- phase A: one local solve per member ----
+        unsigned long long a_dec = 0;
+        for (uint32_t i0 = gt - lane; i0 < m; i0 += GT) {
+            const uint32_t i = i0 + lane;
+            const bool live = i < m;
+            bool dec = false;
+            uint32_t wi = 0, bit = 0;
+            if (live) {
+                const uint32_t c = __ldcg(ML + i);
+                const uint32_t rw = fdiv(c, p.fnx);
+                const uint32_t x = c - rw * nx;
+                uint32_t y, z = 0;
+                if (DIM == 3) {
+                    z = fdiv(rw, p.fny);
+                    y = rw - z * ny;
+                } else {
+                    y = rw;
+                }
+                Sten s;
+                s.c = __ldca(Pc + c);
+                s.w = x > 0 ? __ldca(Pc + (c - 1)) : INFINITY;
+                s.e = x + 1 < nx ? __ldca(Pc + (c + 1)) : INFINITY;
+                s.s = y > 0 ? __ldca(Pc + (c - nx)) : INFINITY;
+                s.n = y + 1 < ny ? __ldca(Pc + (c + nx)) : INFINITY;
+                s.d = s.u = INFINITY;
+                if (DIM == 3) {
+                    s.d = z > 0 ? __ldca(Pc + (c - p.plane32)) : INFINITY;
+                    s.u = z + 1 < nz ? __ldca(Pc + (c + p.plane32)) : INFINITY;
+                }
+                s.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
+                const double v = solve<DIM, SOL>(p, s);
+                dec = v < s.c - p.tol;  // E/ifim.py:203
+                Pn[c] = dec ? v : s.c;
+                wi = rw * p.W + (x >> 5);
+                bit = 1u << (x & 31);
+            }
+            // D_r bits, one atomicOr per distinct word of the warp
+            unsigned pend = __ballot_sync(FULL, dec);
+            a_dec += __popc(pend);
+            while (pend) {
+                const int leader = __ffs(pend) - 1;
+                const uint32_t lw = __shfl_sync(FULL, wi, leader);
+                const bool mine = dec && wi == lw;
+                const uint32_t bits = __reduce_or_sync(FULL, mine ? bit : 0u);
+                if (lane == (unsigned)leader) atomicOr(Dc + lw, bits);
+                pend &= ~__ballot_sync(FULL, mine);
+            }
+        }
+        const unsigned long long td = block_sum(lane == 0 ? a_dec : 0ull, sred);
+        if (threadIdx.x == 0 && td) atomicAdd(&ctl->dsum[r % 3], td);
+        if (!grid_barrier(ctl)) return;
+        const unsigned long long decs = vload(&ctl->dsum[r % 3]);
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->writes += decs;
         if (decs == 0) break;
         if (r + 1 >= (uint32_t)p.cap) {  // E/ifim.py:185-189
-            if (blockIdx.x == 0 && tid == 0) ctl->err = EIK_ECAP;
+            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
             break;
         }
     }
@@ -995,9 +899,8 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
     int64_t N;
     uint32_t W, nwords;
-    uint32_t ntx, nty, ntz, ntiles;
     size_t off_phi2, off_dd, off_bt, off_l0, off_l1;
-    size_t off_tr0, off_td0, off_td1, off_tf, off_ts0, off_ts1, off_tc, off_tl0, off_tl1;
+    size_t off_r0, off_d0, off_d1, off_f;
     size_t off_hist, off_ctl_u, off_ctl_r, total;
     int64_t cap_upd, cap_rem;
 };
@@ -1019,31 +922,20 @@ int make_layout(const eik_geom *g, Layout &L)
     const int64_t nw = W * g->ny * g->nz;
     L.W = (uint32_t)W;
     L.nwords = (uint32_t)nw;
-    const int TY = g->ndim == 3 ? Brick<3>::TY : Brick<2>::TY;
-    const int TZ = g->ndim == 3 ? Brick<3>::TZ : Brick<2>::TZ;
-    L.ntx = (uint32_t)W;
-    L.nty = (uint32_t)((g->ny + TY - 1) / TY);
-    L.ntz = (uint32_t)((g->nz + TZ - 1) / TZ);
-    L.ntiles = L.ntx * L.nty * L.ntz;
     const int64_t s = g->nx + g->ny + (g->ndim == 3 ? g->nz : 0);
     L.cap_upd = 40 * s;  // E/ifim.py:106 (2D: 40*(nx+ny))
     L.cap_rem = 20 * s;  // E/ifim.py:185
-    const size_t tb = (size_t)L.ntiles * TROWS * 4, ti = (size_t)L.ntiles * 4;
+    const size_t bm = (size_t)nw * 4;
     size_t o = 0;
     L.off_phi2 = o; o += al((size_t)L.N * 8);
     L.off_dd = o; o += al((size_t)L.N * 8);
-    L.off_bt = o; o += al((size_t)nw * 4);
-    L.off_l0 = o; o += al((size_t)L.N * 4);
+    L.off_bt = o; o += al(bm);
+    L.off_l0 = o; o += al((size_t)L.N * 4);  // update: active cells; remedy: members
     L.off_l1 = o; o += al((size_t)L.N * 4);
-    L.off_tr0 = o; o += al(tb);
-    L.off_td0 = o; o += al(tb);
-    L.off_td1 = o; o += al(tb);
-    L.off_tf = o; o += al(tb);
-    L.off_ts0 = o; o += al(ti);
-    L.off_ts1 = o; o += al(ti);
-    L.off_tc = o; o += al(ti);
-    L.off_tl0 = o; o += al(ti);
-    L.off_tl1 = o; o += al(ti);
+    L.off_r0 = o; o += al(bm);
+    L.off_d0 = o; o += al(bm);
+    L.off_d1 = o; o += al(bm);
+    L.off_f = o; o += al(bm);
     L.off_hist = o; o += al((size_t)(L.cap_upd + 2) * 8);
     L.off_ctl_u = o; o += al(sizeof(Ctl));
     L.off_ctl_r = o; o += al(sizeof(Ctl));
@@ -1083,18 +975,10 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const doub
     p.hist = (int64_t *)(b + L.off_hist);
     p.hist_cap = L.cap_upd + 2;
     p.cap = cap;
-    p.ntx = L.ntx; p.nty = L.nty; p.ntz = L.ntz; p.ntiles = L.ntiles;
-    p.fntx = make_fastdiv(L.ntx);
-    p.fnty = make_fastdiv(L.nty);
-    p.TR0 = (uint32_t *)(b + L.off_tr0);
-    p.TD0 = (uint32_t *)(b + L.off_td0);
-    p.TD1 = (uint32_t *)(b + L.off_td1);
-    p.TF = (uint32_t *)(b + L.off_tf);
-    p.TS0 = (uint32_t *)(b + L.off_ts0);
-    p.TS1 = (uint32_t *)(b + L.off_ts1);
-    p.TC = (uint32_t *)(b + L.off_tc);
-    p.TL0 = (uint32_t *)(b + L.off_tl0);
-    p.TL1 = (uint32_t *)(b + L.off_tl1);
+    p.R0b = (uint32_t *)(b + L.off_r0);
+    p.D0b = (uint32_t *)(b + L.off_d0);
+    p.D1b = (uint32_t *)(b + L.off_d1);
+    p.Fb = (uint32_t *)(b + L.off_f);
     return p;
 }
 
@@ -1144,7 +1028,6 @@ struct Engine {
     // phi copy (optional), d = delta/F, touched (optional) and the fixed brick bitmap
     static int prep(KP &p, bool copy_phi, bool touched, cudaStream_t st)
     {
-        CK(cudaMemsetAsync(p.TF, 0xff, (size_t)p.ntiles * TROWS * 4, st));
         const int grid = stream_grid(p.nwords);
         if (SOL == SOL_A2) k_prep<DIM, false><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched);
         else k_prep<DIM, true><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched);
@@ -1159,12 +1042,10 @@ struct Engine {
         return EIK_OK;
     }
     static int update(KP &p, cudaStream_t st) { return coop_launch(k_update<DIM, SOL>, p, nullptr, false, st); }
-    // remedy-set slots: R0 bitmap, brick list 0, candidate stamps, counters
+    // remedy-set slots: counters (R0 is rewritten word by word)
     static int reset_set(KP &p, cudaStream_t st)
     {
         CK(cudaMemsetAsync(p.ctl, 0, sizeof(Ctl), st));
-        CK(cudaMemsetAsync(p.TR0, 0, (size_t)p.ntiles * TROWS * 4, st));
-        CK(cudaMemsetAsync(p.TC, 0xff, (size_t)p.ntiles * 4, st));
         return EIK_OK;
     }
     static int build(KP &p, const double *Pc, const unsigned *skip, cudaStream_t st)
@@ -1183,16 +1064,14 @@ struct Engine {
         CK(cudaGetLastError());
         return EIK_OK;
     }
-    static int do_export(KP &p, unsigned n, uint8_t *member, cudaStream_t st)
+    static int do_export(KP &p, uint8_t *member, cudaStream_t st)
     {
-        if (n) k_remedy_export<DIM><<<(int)std::min<unsigned>(n, 4096u), BLOCK, 0, st>>>(p, n, member);
+        k_remedy_export<DIM><<<stream_grid(p.nwords), BLOCK, 0, st>>>(p, member);
         CK(cudaGetLastError());
         return EIK_OK;
     }
     static int remedy(KP &p, const unsigned *skip, cudaStream_t st)
     {
-        CK(cudaMemsetAsync(p.TS0, 0xff, (size_t)p.ntiles * 4, st));
-        CK(cudaMemsetAsync(p.TS1, 0xff, (size_t)p.ntiles * 4, st));
         return coop_launch(k_remedy<DIM, SOL>, p, skip, true, st);
     }
 };
@@ -1291,7 +1170,7 @@ const char *eik_last_error(void) { return g_err.c_str(); }
 
 const char *eik_version(void)
 {
-    return "eik_ifim 0.2 (sm_100a, float64 bit-exact; persistent update worklist + brick-staged remedy)";
+    return "eik_ifim 0.3 (sm_100a, float64 bit-exact; persistent cell-worklist update + member-list remedy)";
 }
 
 int eik_workspace_size(const eik_geom *g, size_t *bytes)
@@ -1414,7 +1293,7 @@ int eik_remedy_export(const eik_geom *g, void *workspace, size_t workspace_bytes
     CK(cudaStreamSynchronize(st));
     CK(cudaMemsetAsync(member, 0, (size_t)L.N, st));
     KP p = make_kp(g, L, workspace, nullptr, nullptr, nullptr, 1e-12, nullptr, 0);
-    rc = dispatch(g, [&](auto E) { return E.do_export(p, c.len[0], member, st); });
+    rc = dispatch(g, [&](auto E) { return E.do_export(p, member, st); });
     if (rc) return rc;
     CK(cudaStreamSynchronize(st));
     return EIK_OK;
