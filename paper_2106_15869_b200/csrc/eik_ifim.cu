@@ -164,51 +164,47 @@ __device__ __forceinline__ double upd2a(double a, double b, double f, double dx,
 }
 
 // E/local_solver.py:91-157 (update_3d_uniform), verified branch walk; d = delta / f.
-// Each branch's root is a pure function of the sorted neighbours and d, so the
-// three candidate roots are evaluated once, without divergence, and the
-// reference's walk (guard, demote/promote, visited set) then runs as predicate
-// logic over them.  Same expressions, same operation order: bit-identical.
+//
+// Every branch's root is a pure function of the sorted neighbours and d, and
+// the walk only compares those roots with the neighbours, so its outcome can
+// be written in closed form.  With F3/F2 = "branch 3/2 demotes on its
+// discriminant (or a2 = inf)", G3 = r3 >= a3, L2 = r2 < a2, H2 = r2 > a3,
+// H1 = r1 > a2, and k0 the guard's entry branch, the walk returns
+//   k0 = 3:  (!F3 && G3) ? r3 : (F2 || L2) ? r1 : r2
+//   k0 = 2:  (F2 || L2) ? r1 : M2
+//   k0 = 1:  (!H1 || F2) ? r1 : M2,     M2 = H2 ? (F3 ? r2 : r3) : r2
+// (walk 3 -> 2 -> 1 stops at 1 because 2 was visited; 2 -> 3 accepts r3
+// because 2 was visited, or falls back to 2 which then returns r2; 1 -> 2
+// ignores L2 because 1 was visited).  The selected value is produced by the
+// reference's own expression: bit-identical.  When every lane of the warp
+// takes the common "k0 = 3 and r3 valid" exit, branch 2 is not evaluated.
 __device__ __forceinline__ double upd3u(double px, double py, double pz, double d, double delta)
 {
     double a1 = px, a2 = py, a3 = pz, t;
     if (a2 < a1) { t = a1; a1 = a2; a2 = t; }
     if (a3 < a2) { t = a2; a2 = a3; a3 = t; }
     if (a2 < a1) { t = a1; a1 = a2; a2 = t; }
-    // k = 1
-    const double r1 = a1 + d;
-    // k = 2 (E/local_solver.py:136-151)
-    const double diff = a2 - a1;
-    const double disc2 = 2.0 * d * d - diff * diff;
-    const bool fail2 = (a2 == INFINITY) || (disc2 < -DISC_CLAMP * (2.0 * d * d));
-    const double r2 = 0.5 * (a1 + a2 + sqrt(disc2 > 0.0 ? disc2 : 0.0));
-    // k = 3 (E/local_solver.py:119-134)
+    const int k0 = (a3 - a1 < delta) ? 3 : ((a2 - a1 < delta) ? 2 : 1);
+    // branch 3 (E/local_solver.py:119-134)
+    const double b2 = a2 - a1;
     const double b3 = a3 - a1;
-    const double s3 = diff + b3;
-    const double disc3 = s3 * s3 - 3.0 * (diff * diff + b3 * b3 - d * d);
-    const bool fail3 = disc3 < -DISC_CLAMP * (3.0 * d * d);
+    const double s3 = b2 + b3;
+    const double disc3 = s3 * s3 - 3.0 * (b2 * b2 + b3 * b3 - d * d);
+    const bool F3 = disc3 < -DISC_CLAMP * (3.0 * d * d);
     const double r3 = a1 + (s3 + sqrt(disc3 > 0.0 ? disc3 : 0.0)) / 3.0;
-    int k = (a3 - a1 < delta) ? 3 : ((a2 - a1 < delta) ? 2 : 1);
-    unsigned vis = 0;
-    double out = r1;
-#pragma unroll 1
-    for (int step = 0; step < 8; ++step) {
-        vis |= 1u << k;
-        if (k == 3) {
-            if (fail3) { k = 2; continue; }
-            if (r3 >= a3 || (vis & 4u)) { out = r3; break; }
-            k = 2;
-        } else if (k == 2) {
-            if (fail2) { k = 1; continue; }
-            if (r2 < a2 && !(vis & 2u)) { k = 1; continue; }
-            if (r2 > a3 && !(vis & 8u)) { k = 3; continue; }
-            out = r2;
-            break;
-        } else {
-            if (r1 > a2 && !(vis & 4u)) { k = 2; continue; }
-            out = r1;
-            break;
-        }
-    }
+    const bool quick = (a1 == INFINITY) || (k0 == 3 && !F3 && r3 >= a3);
+    if (__all_sync(__activemask(), quick)) return a1 == INFINITY ? INFINITY : r3;
+    // branch 2 (E/local_solver.py:136-151) and branch 1 (:152-157)
+    const double disc2 = 2.0 * d * d - b2 * b2;
+    const bool F2 = (a2 == INFINITY) || (disc2 < -DISC_CLAMP * (2.0 * d * d));
+    const double r2 = 0.5 * (a1 + a2 + sqrt(disc2 > 0.0 ? disc2 : 0.0));
+    const double r1 = a1 + d;
+    const bool L2 = r2 < a2, H2 = r2 > a3, H1 = r1 > a2;
+    const double M2 = H2 ? (F3 ? r2 : r3) : r2;
+    double out;
+    if (k0 == 3) out = (!F3 && r3 >= a3) ? r3 : ((F2 || L2) ? r1 : r2);
+    else if (k0 == 2) out = (F2 || L2) ? r1 : M2;
+    else out = (!H1 || F2) ? r1 : M2;
     return a1 == INFINITY ? INFINITY : out;
 }
 
@@ -382,6 +378,12 @@ __device__ __forceinline__ double solve(const KP &p, const Sten &s)
     return upd3u(xm, ym, dmin(s.d, s.u), s.k, p.delta);
 }
 
+// Worklist entries: cell index | CARRY.  CARRY marks cells that changed in the
+// previous iteration/round; only they must rewrite an unchanged value into the
+// other phi buffer to keep the Jacobi double buffer consistent (every other
+// cell already holds its current value there).  Cell indices are < 2^31.
+constexpr uint32_t CARRY = 0x80000000u;
+
 // Block-wide exclusive scan of a per-thread count plus one global reservation:
 // returns this thread's first slot in the global list whose length is *glen.
 __device__ __forceinline__ unsigned block_reserve(unsigned v, unsigned *glen, unsigned *sscan)
@@ -522,8 +524,11 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
             const unsigned i = base + threadIdx.x;
             uint32_t c = 0, x = 0, y = 0, z = 0, r = 0;
             unsigned emit = 0;  // bit 0: stay; bits 1..6: activate W, E, S, N, D, U
+            bool carry = false;
             if (i < n) {
                 c = __ldcg(Lc + i);
+                carry = (c & CARRY) != 0;  // non-converged in the previous iteration
+                c &= ~CARRY;
                 r = fdiv(c, p.fnx);
                 x = c - r * nx;
                 if (DIM == 3) {
@@ -547,7 +552,8 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
                 const double v = solve<DIM, SOL>(p, s);
                 // E/ifim.py:121: converged iff v == old or |v - old| <= tol
                 const bool conv = (v == s.c) || fabs(v - s.c) <= p.tol;
-                Pn[c] = conv ? s.c : v;  // E/ifim.py:128 (+ double-buffer carry)
+                if (!conv) Pn[c] = v;           // E/ifim.py:128
+                else if (carry) Pn[c] = s.c;    // changed last iteration: carry into the other buffer
                 if (!conv) {
                     emit = 1u;
                     ++a_writes;
@@ -574,7 +580,7 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
                 }
             }
             unsigned pos = block_reserve(__popc(emit), lenN, sscan);
-            if (emit & 1u) Ln[pos++] = c;
+            if (emit & 1u) Ln[pos++] = c | CARRY;
 #pragma unroll
             for (int k = 0; k < (DIM == 3 ? 6 : 4); ++k) {
                 const uint32_t e = k == 0 ? c - 1 : k == 1 ? c + 1 : k == 2 ? c - nx : k == 3 ? c + nx
@@ -700,19 +706,21 @@ __global__ void k_remedy_export(KP p, uint8_t *member)
 
 constexpr int REM_PER = 4;  // bitmap words per thread in phase B
 
+
 template <int DIM>
 __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint32_t *__restrict__ Dp,
                                             uint32_t *Dc, uint32_t *ML, unsigned *lenR, unsigned *sscan)
 {
+    const unsigned lane = lane_id();
     const uint32_t chunk = BLOCK * REM_PER;
     const uint32_t planeW = (uint32_t)p.ny * p.W;
     for (uint32_t base = blockIdx.x * chunk; base < p.nwords; base += gridDim.x * chunk) {
-        uint32_t R[REM_PER];
+        uint32_t R[REM_PER], C[REM_PER];
         unsigned cnt = 0;
 #pragma unroll
         for (int k = 0; k < REM_PER; ++k) {
             const uint32_t w = base + threadIdx.x + k * BLOCK;
-            R[k] = 0;
+            R[k] = C[k] = 0;
             if (w < p.nwords) {
                 if (r == 0) {
                     R[k] = __ldcg(p.R0b + w);
@@ -739,24 +747,31 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
                     }
                     const uint32_t dil = (c << 1) | (c >> 1) | (dw >> 31) | (de << 31) | ds | dn | dd | du;
                     R[k] = c | (dil & ~__ldg(p.Fb + w));
+                    C[k] = c;
                 }
                 Dc[w] = 0;  // D_r is accumulated by phase A with atomicOr
                 cnt += __popc(R[k]);
             }
         }
         unsigned pos = block_reserve(cnt, lenR, sscan);
+        // warp-cooperative expansion: one word at a time, 32 coalesced entries per store
 #pragma unroll
         for (int k = 0; k < REM_PER; ++k) {
-            uint32_t b = R[k];
-            if (!b) continue;
+            unsigned todo = __ballot_sync(FULL, R[k] != 0);
             const uint32_t w = base + threadIdx.x + k * BLOCK;
             const uint32_t row = fdiv(w, p.fW);
             const uint32_t c0 = row * p.nx32 + (w - row * p.W) * 32u;
-            while (b) {
-                const uint32_t x = __ffs(b) - 1;
-                b &= b - 1;
-                ML[pos++] = c0 + x;
+            while (todo) {
+                const int src = __ffs(todo) - 1;
+                todo &= todo - 1;
+                const uint32_t bits = __shfl_sync(FULL, R[k], src);
+                const uint32_t carry = __shfl_sync(FULL, C[k], src);
+                const uint32_t off = __shfl_sync(FULL, pos, src);
+                const uint32_t cc0 = __shfl_sync(FULL, c0, src);
+                if ((bits >> lane) & 1u)
+                    ML[off + __popc(bits & ((1u << lane) - 1u))] = (cc0 + lane) | (((carry >> lane) & 1u) ? CARRY : 0u);
             }
+            pos += __popc(R[k]);
         }
     }
 }
@@ -801,13 +816,16 @@ __global__ void __launch_bounds__(BLOCK, 4) k_remedy(KP p, const unsigned *skip)
         }
         // ---- phase A: one local solve per member ----
         unsigned long long a_dec = 0;
+        uint32_t nxt = (gt < m) ? __ldcg(ML + gt) : 0u;
         for (uint32_t i0 = gt - lane; i0 < m; i0 += GT) {
             const uint32_t i = i0 + lane;
             const bool live = i < m;
+            const uint32_t ent = nxt;
+            if (i + GT < m) nxt = __ldcg(ML + i + GT);  // prefetch the next member
             bool dec = false;
             uint32_t wi = 0, bit = 0;
             if (live) {
-                const uint32_t c = __ldcg(ML + i);
+                const uint32_t c = ent & ~CARRY;
                 const uint32_t rw = fdiv(c, p.fnx);
                 const uint32_t x = c - rw * nx;
                 uint32_t y, z = 0;
@@ -831,7 +849,8 @@ __global__ void __launch_bounds__(BLOCK, 4) k_remedy(KP p, const unsigned *skip)
                 s.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
                 const double v = solve<DIM, SOL>(p, s);
                 dec = v < s.c - p.tol;  // E/ifim.py:203
-                Pn[c] = dec ? v : s.c;
+                if (dec) Pn[c] = v;
+                else if (ent & CARRY) Pn[c] = s.c;  // changed last round: carry into the other buffer
                 wi = rw * p.W + (x >> 5);
                 bit = 1u << (x & 31);
             }
