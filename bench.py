@@ -1,0 +1,333 @@
+#!/usr/bin/env python
+"""Benchmark of the iFIM hot path (BASELINE.json metric: grid-node updates/s and
+wall-clock to convergence, 3D 512^3).
+
+Workload: 3D 512^3, h = 1, checkerboard speed of 32^3
+blocks, F = 1 where (i//32 + j//32 + k//32) is even else 0.01 (the paper's 1:100
+ratio), one point seed (value 0) at the centre (256, 256, 256).
+
+A step = one complete solve_ifim (update step + build pass + remedy step) on a
+fresh field: phi = +inf and state = FAR/BLOCKED are restored from resident
+device copies at the start of every step (inside the timed region).
+Node updates = RunStats.solver_calls (identical to the reference's count,
+SURVEY.md §8d).  `value` = total node updates / device time over all ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--size 512] [--impl ours|reference]
+
+N > 1 (torchrun): every rank solves its own full 512^3 instance (independent
+replicas, weak scaling); the time is the max over ranks.  --impl reference
+times the CPU oracle port of the reference algorithm (oracle/eik_oracle.c,
+OpenMP on all host cores) on a bounded sample of the same workload family.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+PEAKS_FILE = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+METRIC = "grid-node updates/sec (and wall-clock to convergence), 3D 512^3"
+UNIT = "node-updates/s"
+
+
+def checker_speed_np(n: int, blk: int) -> np.ndarray:
+    k = np.arange(n) // blk
+    return np.where(((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2) == 0, 1.0, 0.01)
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_FILE) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def traffic_from_profiles(workload: str):
+    """dram bytes per launch of k_remedy from the committed ncu --set full summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        e = d.get("kernels", {}).get("k_remedy", {})
+        if e.get("workload") == workload:
+            return float(e["dram_bytes_read"]) + float(e["dram_bytes_write"])
+    except Exception:
+        pass
+    return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        if not self.path or not os.path.exists(self.path):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as fh:
+            for line in fh:
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 9:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx.append(float(f[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, f[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [x for x in sm if x > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_sample(n: int, threads: int):
+    """Oracle port (C, OpenMP) on the same workload family at n^3; returns (calls, seconds)."""
+    from oracle import cpu
+
+    cpu.build()
+    F = checker_speed_np(n, max(1, n // 16))
+    c = n // 2
+    t0 = time.perf_counter()
+    res = cpu.solve_ifim((n, n, n), 1.0, F, [(c * n + c) * n + c], [0.0], threads=threads)
+    dt = time.perf_counter() - t0
+    return res.stats["solver_calls"], dt
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    n = args.cpu_size
+    for _ in range(args.warmup):
+        cpu_sample(n, threads)
+    calls, secs = 0, 0.0
+    for _ in range(args.steps):
+        c, s = cpu_sample(n, threads)
+        calls += c
+        secs += s
+    v = calls / secs
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"cfg4 family: 3D {n}^3 checkerboard 1:100 ({max(1, n // 16)}^3 blocks), centre seed "
+                               f"(bounded CPU sample of the 512^3 workload)", "size": n, "parallelism": "host threads"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"full solve_ifim of the {n}^3 checkerboard (same family), "
+                                   f"oracle/eik_oracle.c OpenMP x{threads}"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+
+    world, rank, local = dist_setup()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2106_15869_b200 as eik
+
+    n = args.size
+    blk = max(1, n // 16)
+    c = n // 2
+    workload = f"cfg4: 3D {n}^3 checkerboard 1:100 ({blk}^3 blocks), h=1, seed (c,c,c)"
+    # resident inputs
+    kk = torch.arange(n, device=dev) // blk
+    F = torch.where(((kk[:, None, None] + kk[None, :, None] + kk[None, None, :]) % 2) == 0, 1.0, 0.01).double()
+    phi0 = torch.full((n, n, n), float("inf"), dtype=torch.float64, device=dev)
+    st0 = torch.zeros((n, n, n), dtype=torch.uint8, device=dev)
+    phi = torch.empty_like(phi0)
+    st = torch.empty_like(st0)
+    g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), phi, F, st)
+    bc = eik.BoundaryCondition(((eik.CellIndex3D(c, c, c), 0.0),))
+
+    def step():
+        phi.copy_(phi0)
+        st.copy_(st0)
+        return eik.solve_ifim(g, bc)
+
+    for _ in range(args.warmup):
+        res = step()
+    torch.cuda.synchronize()
+    calls = res.stats.solver_calls
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    rem_ms = []
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        launches = 0
+        for _ in range(args.steps):
+            r = step()
+            rem_ms.append(r.stats.device_ms["remedy"])
+            launches += r.stats.gpu_launches
+            assert r.stats.solver_calls == calls
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = calls * args.steps * world / (ms / 1e3)
+    clocks = clk.summary()
+
+    # roofline of the dominant kernel (k_remedy): algorithmic bytes (SURVEY.md §8d:
+    # 8 B x (2 x solver_calls + phi_writes), remedy phase) / CUDA-event duration
+    ph = r.stats.phases
+    rem_calls = ph["remedy"]["solver_calls"]
+    rem_writes = r.stats.phi_writes - (ph["update"]["solver_calls"] - ph["update"]["converged"])
+    alg_bytes = 8.0 * (2 * rem_calls + rem_writes)
+    rem_s = statistics.median(rem_ms) / 1e3
+    peak, peak_src = hbm_peak()
+    achieved = alg_bytes / rem_s / 1e9
+    traffic = traffic_from_profiles(workload)
+
+    out = None
+    if rank == 0:
+        # end to end through the public API with host (pinned) buffers
+        e2e = run_e2e(eik, torch, dev, n, blk, c, F.cpu().numpy(), calls, args)
+        cpu_calls, cpu_s = cpu_sample(args.cpu_size, os.cpu_count() or 1) if not args.no_cpu else (0, 0.0)
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload, "size": n, "solver_calls_per_step": calls,
+                       "iterations": r.stats.iterations, "peak_remedy": r.stats.peak_remedy,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (phi 1 GiB fp64 per field at 512^3)",
+                       "phase_ms": {k: round(v, 3) for k, v in r.stats.device_ms.items()}},
+            "wall_clock_to_convergence_ms": ms / args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "kernel": "k_remedy", "alg_bytes_per_launch": alg_bytes,
+                         "launch_ms": rem_s * 1e3, "peak_source": peak_src},
+            "cpu_baseline": {"value": (cpu_calls / cpu_s) if cpu_s else None, "unit": UNIT,
+                             "cores": os.cpu_count() or 1, "kind": "port",
+                             "sample": f"full solve of the {args.cpu_size}^3 checkerboard (same family) with "
+                                       f"oracle/eik_oracle.c, OpenMP x{os.cpu_count() or 1}, {cpu_s:.1f} s"},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+    if out is not None:
+        print(json.dumps(out), flush=True)
+    return 0
+
+
+def run_e2e(eik, torch, dev, n, blk, c, F_host, calls, args):
+    """Same metric through solve_ifim with host buffers: H2D of phi/speed/state from pinned
+    memory and D2H of phi inside each timed step."""
+    speed = torch.from_numpy(F_host).pin_memory()
+    phi = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
+    state = torch.empty((n, n, n), dtype=torch.uint8).pin_memory()
+    bc = eik.BoundaryCondition(((eik.CellIndex3D(c, c, c), 0.0),))
+    steps = max(1, min(args.steps, 3))
+    tot = 0.0
+    for it in range(steps + 1):
+        phi.fill_(float("inf"))
+        state.zero_()
+        g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), phi, speed, state)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = eik.solve_ifim(g, bc)
+        dt = time.perf_counter() - t0
+        assert res.stats.solver_calls == calls
+        if it > 0:  # first call is a warm-up (allocations)
+            tot += dt
+    N = n ** 3
+    return {"value": calls * steps / tot, "unit": UNIT, "h2d_bytes_per_step": N * (8 + 8 + 1),
+            "d2h_bytes_per_step": N * 8, "steps": steps, "ms_per_step": tot / steps * 1e3}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--size", type=int, default=512)
+    ap.add_argument("--cpu-size", type=int, default=96)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -127,6 +127,13 @@ __device__ __forceinline__ double dmax(double a, double b) { return a >= b ? a :
 // numpy.maximum(x, 0.0): NaN propagates
 __device__ __forceinline__ double npmax0(double x) { return (x != x) ? x : (x >= 0.0 ? x : 0.0); }
 
+// sqrt(max(x, 0)) for the roots: x <= 0 (or NaN) yields +0 without feeding the
+// IEEE slow path (sqrt of 0/negative/NaN); the reference's clamp
+// `x if x > 0 else 0` (E/local_solver.py) gives exactly +0 there too.  Where
+// the numpy form would propagate NaN (E/_kernels.py:56, NaN disc) the root is
+// never selected (take_two / isfinite guards), so the result is unchanged.
+__device__ __forceinline__ double sqrt_pos(double x) { return x > 0.0 ? sqrt(x > 0.0 ? x : 1.0) : 0.0; }
+
 // E/_kernels.py:47-58 (_update_uniform_batch), d = delta / f
 __device__ __forceinline__ double upd2u(double a, double b, double d)
 {
@@ -136,7 +143,7 @@ __device__ __forceinline__ double upd2u(double a, double b, double d)
     const double diff = hi - lo;
     const bool take_two = diff <= kSqrt2 * d;
     const double disc = 2.0 * d * d - diff * diff;
-    const double root = 0.5 * (a + b + sqrt(npmax0(disc)));
+    const double root = 0.5 * (a + b + sqrt_pos(disc));
     const bool valid = take_two && (disc >= -DISC_CLAMP * (2.0 * d * d)) && (root >= hi);
     return valid ? root : one;
 }
@@ -152,7 +159,7 @@ __device__ __forceinline__ double upd2a(double a, double b, double f, double dx,
     const double s = sqrt(s2);
     const double diff = a - b;
     const double disc = s2 - diff * diff;
-    const double root = (a * dy2 + b * dx2 + (dx * dy) * sqrt(npmax0(disc))) / (dx2 + dy2);
+    const double root = (a * dy2 + b * dx2 + (dx * dy) * sqrt_pos(disc)) / (dx2 + dy2);
     const double drop_larger = (a > b) ? one_y : one_x;
     const bool valid = isfinite(a) && isfinite(b) && !(diff > s) && !(-diff > s) &&
                        (disc >= -DISC_CLAMP * s2) && (root >= a) && (root >= b);
@@ -191,13 +198,16 @@ __device__ __forceinline__ double upd3u(double px, double py, double pz, double 
     const double s3 = b2 + b3;
     const double disc3 = s3 * s3 - 3.0 * (b2 * b2 + b3 * b3 - d * d);
     const bool F3 = disc3 < -DISC_CLAMP * (3.0 * d * d);
-    const double r3 = a1 + (s3 + sqrt(disc3 > 0.0 ? disc3 : 0.0)) / 3.0;
+    // r3 is only ever selected with a3 finite; an infinite dividend would take
+    // the division slow path for a value nobody reads
+    const double x3 = s3 + sqrt_pos(disc3);
+    const double r3 = a1 + (x3 < INFINITY ? x3 : 0.0) / 3.0;
     const bool quick = (a1 == INFINITY) || (k0 == 3 && !F3 && r3 >= a3);
     if (__all_sync(__activemask(), quick)) return a1 == INFINITY ? INFINITY : r3;
     // branch 2 (E/local_solver.py:136-151) and branch 1 (:152-157)
     const double disc2 = 2.0 * d * d - b2 * b2;
     const bool F2 = (a2 == INFINITY) || (disc2 < -DISC_CLAMP * (2.0 * d * d));
-    const double r2 = 0.5 * (a1 + a2 + sqrt(disc2 > 0.0 ? disc2 : 0.0));
+    const double r2 = 0.5 * (a1 + a2 + sqrt_pos(disc2));
     const double r1 = a1 + d;
     const bool L2 = r2 < a2, H2 = r2 > a3, H1 = r1 > a2;
     const double M2 = H2 ? (F3 ? r2 : r3) : r2;
@@ -719,7 +729,7 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
         unsigned cnt = 0;
 #pragma unroll
         for (int k = 0; k < REM_PER; ++k) {
-            const uint32_t w = base + threadIdx.x + k * BLOCK;
+            const uint32_t w = base + threadIdx.x * REM_PER + k;  // consecutive words: list stays word-sorted
             R[k] = C[k] = 0;
             if (w < p.nwords) {
                 if (r == 0) {
@@ -758,7 +768,7 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
 #pragma unroll
         for (int k = 0; k < REM_PER; ++k) {
             unsigned todo = __ballot_sync(FULL, R[k] != 0);
-            const uint32_t w = base + threadIdx.x + k * BLOCK;
+            const uint32_t w = base + threadIdx.x * REM_PER + k;
             const uint32_t row = fdiv(w, p.fW);
             const uint32_t c0 = row * p.nx32 + (w - row * p.W) * 32u;
             while (todo) {
@@ -854,17 +864,20 @@ __global__ void __launch_bounds__(BLOCK, 4) k_remedy(KP p, const unsigned *skip)
                 wi = rw * p.W + (x >> 5);
                 bit = 1u << (x & 31);
             }
-            // D_r bits, one atomicOr per distinct word of the warp
-            unsigned pend = __ballot_sync(FULL, dec);
-            a_dec += __popc(pend);
-            while (pend) {
-                const int leader = __ffs(pend) - 1;
-                const uint32_t lw = __shfl_sync(FULL, wi, leader);
-                const bool mine = dec && wi == lw;
-                const uint32_t bits = __reduce_or_sync(FULL, mine ? bit : 0u);
-                if (lane == (unsigned)leader) atomicOr(Dc + lw, bits);
-                pend &= ~__ballot_sync(FULL, mine);
+            // D_r bits: a warp's members of one word are contiguous in the list, so a
+            // segmented OR-scan leaves each word's bits in its first lane, which
+            // issues a single atomicOr for the word.
+            a_dec += __popc(__ballot_sync(FULL, dec));
+            if (!live) wi = 0xffffffffu;
+            uint32_t acc = dec ? bit : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t ov = __shfl_down_sync(FULL, acc, o);
+                const uint32_t ow = __shfl_down_sync(FULL, wi, o);
+                if (lane + o < 32 && ow == wi) acc |= ov;
             }
+            const uint32_t pw = __shfl_up_sync(FULL, wi, 1);
+            if (live && acc && (lane == 0 || pw != wi)) atomicOr(Dc + wi, acc);
         }
         const unsigned long long td = block_sum(lane == 0 ? a_dec : 0ull, sred);
         if (threadIdx.x == 0 && td) atomicAdd(&ctl->dsum[r % 3], td);

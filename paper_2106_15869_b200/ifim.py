@@ -94,7 +94,8 @@ class _DeviceGrid:
                 raise ValueError("grid arrays live on different devices")
             return arr
         t = torch.as_tensor(np.ascontiguousarray(arr)) if isinstance(arr, np.ndarray) else arr
-        return t.to(device=self.device, dtype=dtype).contiguous()
+        pinned = isinstance(t, torch.Tensor) and t.is_pinned()
+        return t.to(device=self.device, dtype=dtype, non_blocking=pinned).contiguous()
 
     @property
     def stream(self):
@@ -114,7 +115,9 @@ def _copy_into(host_arr, dev_t):
     if isinstance(host_arr, np.ndarray):
         torch.from_numpy(host_arr).copy_(dev_t.reshape(host_arr.shape))
     else:
-        host_arr.copy_(dev_t.reshape(host_arr.shape))
+        host_arr.copy_(dev_t.reshape(host_arr.shape), non_blocking=host_arr.is_pinned())
+        if host_arr.is_pinned():
+            torch.cuda.current_stream(dev_t.device).synchronize()
 
 
 def _host_mark_sources(grid, idx):
