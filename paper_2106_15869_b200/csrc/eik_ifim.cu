@@ -52,7 +52,7 @@ constexpr uint8_t ST_SOURCE = 2, ST_BLOCKED = 4;  // E/grid.py:21-26
 enum { SOL_U2 = 0, SOL_A2 = 1, SOL_U3 = 2 };
 
 // E/_kernels.py:18 (math.sqrt(2.0)) and E/local_solver.py:28
-__device__ __constant__ double kSqrt2 = 1.4142135623730951;
+constexpr double kSqrt2 = 1.4142135623730951;
 #define DISC_CLAMP 1e-12
 
 struct Ctl {
@@ -124,15 +124,19 @@ struct KP {
 
 __device__ __forceinline__ double dmin(double a, double b) { return a <= b ? a : b; }
 __device__ __forceinline__ double dmax(double a, double b) { return a >= b ? a : b; }
-// numpy.maximum(x, 0.0): NaN propagates
-__device__ __forceinline__ double npmax0(double x) { return (x != x) ? x : (x >= 0.0 ? x : 0.0); }
 
 // sqrt(max(x, 0)) for the roots: x <= 0 (or NaN) yields +0 without feeding the
 // IEEE slow path (sqrt of 0/negative/NaN); the reference's clamp
 // `x if x > 0 else 0` (E/local_solver.py) gives exactly +0 there too.  Where
 // the numpy form would propagate NaN (E/_kernels.py:56, NaN disc) the root is
 // never selected (take_two / isfinite guards), so the result is unchanged.
-__device__ __forceinline__ double sqrt_pos(double x) { return x > 0.0 ? sqrt(x > 0.0 ? x : 1.0) : 0.0; }
+__device__ __forceinline__ double sqrt_rn(double x)
+{
+    double r;  // opaque to the optimizer, so the operand select below is not folded away
+    asm("sqrt.rn.f64 %0, %1;" : "=d"(r) : "d"(x));
+    return r;
+}
+__device__ __forceinline__ double sqrt_pos(double x) { return x > 0.0 ? sqrt_rn(x > 0.0 ? x : 1.0) : 0.0; }
 
 // E/_kernels.py:47-58 (_update_uniform_batch), d = delta / f
 __device__ __forceinline__ double upd2u(double a, double b, double d)
