@@ -1,0 +1,88 @@
+"""C ABI (include/eik_ifim.h) checks that need no GPU: the library loads, exports
+every declared symbol, validates geometry, and the host-side index math is exact."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2106_15869_b200 import _native
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "eik_ifim.h")).read()
+    return sorted(set(re.findall(r"^\w[\w\s\*]*?\b(eik_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.lib()
+    names = declared_functions()
+    assert len(names) >= 10
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(_native.EXPORTS)
+    assert b"sm_100a" in lib.eik_version()
+
+
+def test_library_is_built_for_sm100a():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _native.LIB], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_workspace_size_and_validation():
+    lib = _native.lib()
+    n = C.c_size_t(0)
+    g = _native.Geom(512, 512, 512, 1.0, 1.0, 1.0, 3, 0)
+    assert lib.eik_workspace_size(C.byref(g), C.byref(n)) == 0
+    N = 512 ** 3
+    assert n.value >= N * (8 + 8 + 4 + 4)  # phi copy, d, two cell lists
+    assert n.value < N * 40
+    bad = [
+        _native.Geom(8, 8, 8, 1.0, 1.0, 2.0, 3, 0),   # anisotropic 3D
+        _native.Geom(8, 8, 2, 1.0, 1.0, 1.0, 2, 0),   # 2D with nz != 1
+        _native.Geom(0, 8, 1, 1.0, 1.0, 1.0, 2, 0),   # empty
+        _native.Geom(8, 8, 1, -1.0, 1.0, 1.0, 2, 0),  # negative spacing
+        _native.Geom(8, 8, 1, 1.0, 1.0, 1.0, 4, 0),   # ndim
+        _native.Geom(2048, 2048, 1024, 1.0, 1.0, 1.0, 3, 0),  # > 2^31 cells
+    ]
+    for g in bad:
+        assert lib.eik_workspace_size(C.byref(g), C.byref(n)) == _native.EIK_EINVAL
+        assert lib.eik_last_error()
+
+
+def test_null_arguments_rejected_without_touching_the_gpu():
+    lib = _native.lib()
+    g = _native.Geom(8, 8, 1, 1.0, 1.0, 1.0, 2, 0)
+    st = _native.Stats()
+    rc = lib.eik_ifim_solve(C.byref(g), None, None, None, None, None, 0, 1e-12, None, 0, None, 0, C.byref(st), None)
+    assert rc == _native.EIK_EINVAL
+    rc = lib.eik_local_solve(7, None, None, None, None, 1.0, 1.0, None, 1, None)
+    assert rc == _native.EIK_EINVAL
+
+
+def _fastdiv(d):
+    """Host restatement of make_fastdiv / fdiv in eik_ifim.cu (round-up multiplier)."""
+    if d <= 1:
+        return lambda n: n
+    l = (d - 1).bit_length()
+    p = 31 + l
+    mul = ((1 << p) + d - 1) // d
+    shr = p - 32
+    return lambda n: ((n * mul) >> 32) >> shr
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 7, 16, 17, 24, 33, 48, 53, 100, 256, 511, 512, 1000, 1023, 1024, 4095,
+                               4096, 65535, 131071])
+def test_fastdiv_exact_below_2_31(d):
+    f = _fastdiv(d)
+    rng = np.random.default_rng(d)
+    ns = np.concatenate([rng.integers(0, 2 ** 31, 20000), np.arange(0, 5000), 2 ** 31 - 1 - np.arange(2000),
+                         np.arange(1, 2000) * d - 1, np.arange(1, 2000) * d])
+    for n in ns.tolist():
+        if n < 2 ** 31:
+            assert f(n) == n // d, (n, d)

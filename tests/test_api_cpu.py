@@ -1,0 +1,127 @@
+"""Host-side API semantics of the drop-in boundary (no GPU needed): grid and
+boundary conventions mirror E/grid.py, validation happens before anything is
+written, and the product path refuses to run without a CUDA device."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2106_15869_b200 as eik
+
+
+def test_new_grid_conventions():
+    """E/grid.py:108-144."""
+    F = np.ones((3, 4))
+    F[1, 2] = 0.0
+    g = eik.new_grid(4, 3, 0.5, 0.25, origin=(1.0, 2.0), speed=F)
+    assert g.shape == (3, 4) and g.phi.shape == (3, 4)
+    assert np.isinf(g.phi).all()
+    assert g.state[1, 2] == eik.CellState.BLOCKED and g.state[0, 0] == eik.CellState.FAR
+    assert g.cell_center(2, 1) == (2.0, 2.25)
+    assert eik.CellIndex(2, 1).linear(4) == 6
+    with pytest.raises(ValueError):
+        eik.new_grid(4, 3, 1.0, 1.0, speed=-np.ones((3, 4)))
+    with pytest.raises(ValueError):
+        eik.new_grid(4, 3, 0.0, 1.0)
+    with pytest.raises(ValueError):
+        eik.new_grid(4, 3, 1.0, 1.0, speed=np.ones((4, 3)))
+    g = eik.new_grid(5, 4, 1.0, 1.0, speed=lambda x, y: x + y + 1.0)
+    assert g.speed[3, 4] == 8.0
+
+
+def test_new_grid_3d_conventions():
+    F = np.ones((2, 3, 4))
+    F[1, 2, 3] = 0.0
+    g = eik.new_grid_3d(4, 3, 2, 0.5, speed=F)
+    assert g.shape == (2, 3, 4) and g.dx == g.dy == g.dz == 0.5
+    assert g.state[1, 2, 3] == eik.CellState.BLOCKED
+    assert eik.CellIndex3D(3, 2, 1).linear(4, 3) == 23
+    g = eik.new_grid_3d(3, 3, 3, 1.0, speed=lambda x, y, z: 1.0 + z)
+    assert g.speed[2, 0, 0] == 3.0
+
+
+def test_boundary_condition_validation():
+    """E/grid.py:82-105."""
+    with pytest.raises(ValueError):
+        eik.BoundaryCondition(((eik.CellIndex(0, 0), float("inf")),))
+    with pytest.raises(ValueError):
+        eik.BoundaryCondition(((eik.CellIndex(0, 0), 0.0), ((0, 0), 1.0)))
+    bc = eik.BoundaryCondition((((1, 2), 0.5),)).merged_with(eik.BoundaryCondition((((3, 0), 0.0),)))
+    assert len(bc) == 2 and bc.seeds[0][0] == eik.CellIndex(1, 2)
+    bc3 = eik.BoundaryCondition((((1, 2, 3), 0.0),))
+    assert isinstance(bc3.seeds[0][0], eik.CellIndex3D)
+
+
+def test_seed_validation_happens_before_any_write():
+    """apply_boundary validates every seed before writing (E/grid.py:204-215)."""
+    F = np.ones((5, 5))
+    F[2, 2] = 0.0
+    g = eik.new_grid(5, 5, 1.0, 1.0, speed=F)
+    with pytest.raises(ValueError):
+        eik.seed_linear(g, eik.BoundaryCondition(()))
+    with pytest.raises(ValueError):
+        eik.seed_linear(g, eik.BoundaryCondition((((0, 0), 0.0), ((2, 2), 0.0))))
+    with pytest.raises(ValueError):
+        eik.seed_linear(g, eik.BoundaryCondition((((0, 0), 0.0), ((5, 0), 0.0))))
+    assert np.isinf(g.phi).all()
+    idx, val = eik.seed_linear(g, eik.BoundaryCondition((((1, 3), 0.25),)))
+    assert idx == [16] and val == [0.25]
+    with pytest.raises(ValueError):
+        eik.seed_point(g, (2, 2), 0.0)
+    g3 = eik.new_grid_3d(3, 4, 5, 1.0)
+    assert eik.seed_linear(g3, eik.seed_point(g3, (2, 3, 4), 1.0)) == ([59], [1.0])
+
+
+def test_resolve_workers():
+    """E/parallel.py:28-42."""
+    assert eik.resolve_workers(3) == 3
+    assert eik.resolve_workers(0) >= 1
+    with pytest.raises(ValueError):
+        eik.resolve_workers(-1)
+
+
+def test_run_method_dispatch():
+    g = eik.new_grid(4, 4, 1.0, 1.0)
+    with pytest.raises(ValueError):
+        eik.run_method("fmm", g, eik.seed_point(g, (0, 0), 0.0))
+    assert eik.METHOD_NAMES == ("ifim",)
+
+
+def test_field_helpers_match_reference_semantics():
+    """E/harness.py:165-179."""
+    a = np.array([[0.0, np.inf], [1.0, 2.0]])
+    b = np.array([[0.5, np.inf], [1.0, 1.0]])
+    assert eik.field_max_diff(a, b) == 1.0
+    assert eik.field_max_diff(torch.tensor(a), torch.tensor(a)) == 0.0
+    with pytest.raises(ValueError):
+        eik.field_max_diff(a, b[:1])
+    import hashlib
+
+    assert eik.field_sha256(a) == hashlib.sha256(a.tobytes()).hexdigest()
+
+
+def test_tol_is_validated_first():
+    g = eik.new_grid(8, 8, 1.0, 1.0)
+    for fn in (lambda: eik.solve_ifim(g, eik.seed_point(g, (0, 0), 0.0), tol=-1e-9),
+               lambda: eik.ifim_update_step(g, eik.seed_point(g, (0, 0), 0.0), tol=0.0),
+               lambda: eik.build_remedy_set(g, tol=0.0),
+               lambda: eik.ifim_remedy_step(g, eik.RemedySet(member=np.zeros(64, bool)), tol=-1.0)):
+        with pytest.raises(ValueError):
+            fn()
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
+def test_no_cpu_fallback():
+    g = eik.new_grid(8, 8, 1.0, 1.0)
+    with pytest.raises(RuntimeError, match="CUDA"):
+        eik.solve_ifim(g, eik.seed_point(g, (0, 0), 0.0))
+    assert np.isinf(g.phi).all()
+
+
+def test_remedy_set_host_side():
+    member = np.zeros(16, dtype=bool)
+    member[[3, 7]] = True
+    rs = eik.RemedySet(member=member)
+    assert len(rs) == 2 and rs.cells == [3, 7]
+    rs2 = eik.RemedySet(member=member.copy(), cells=[3, 7])
+    rs2._drain()
+    assert len(rs2) == 0 and not rs2.member.any()
