@@ -45,11 +45,15 @@ extern "C" {
 
 #define EIK_F64 0
 
+#define EIK_GEOM_SLAB 1 /* flags: local z-slab of a sharded 3D grid, planes 0 and nz-1 are ghosts */
+
 typedef struct eik_geom {
     int64_t nx, ny, nz; /* nz = 1 for 2D */
     double dx, dy, dz;  /* 3D requires dx == dy == dz */
     int32_t ndim;       /* 2 or 3 */
     int32_t dtype;      /* EIK_F64 */
+    int32_t flags;      /* EIK_GEOM_SLAB or 0 */
+    int32_t reserved;
 } eik_geom;
 
 /* RunStats (E/result.py:9-18) plus device-side extras. */
@@ -109,6 +113,37 @@ int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t 
  * (a, b, c, f, dx). */
 int eik_local_solve(int kind, const double *a, const double *b, const double *c, const double *f,
                     double dx, double dy, double *out, int64_t n, void *stream);
+
+/* ---- z-slab sharding (protocol in paper_2106_15869_b200/slab.py) ----
+ * The geometry is the rank's local slab with one ghost plane on each side
+ * (flags = EIK_GEOM_SLAB, nz = owned planes + 2).  Every call runs one
+ * bulk-synchronous step on the given stream and returns the LOCAL counts; the
+ * caller exchanges ghost planes / requests / decrease planes and reduces the
+ * counts between steps.  Workspace offsets of the buffers the exchange touches
+ * come from eik_workspace_offsets: [0] second phi buffer (float64), [1] touched
+ * bitmap (update: ghost rows = outgoing activation requests), [2] D0, [3] D1
+ * (remedy decrease bitmaps by round parity); bitmaps have ceil(nx/32) uint32
+ * words per x-row, rows ordered (z, y). */
+int eik_workspace_offsets(const eik_geom *g, int64_t *offsets /* [4] */);
+/* Seeds (local linear indices, owned or ghost planes) + initial activation of
+ * owned cells (E/ifim.py:97-102); *n_active = local |A_1|. */
+int eik_slab_update_init(const eik_geom *g, double *phi, const double *speed, uint8_t *state,
+                         const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
+                         void *workspace, size_t workspace_bytes, int64_t *n_active, void *stream);
+/* Update iteration `it` (0-based; reads phi buffer it&1, writes (it+1)&1). */
+int eik_slab_update_iter(const eik_geom *g, double *phi, const double *speed, uint8_t *state, double tol,
+                         int64_t it, void *workspace, size_t workspace_bytes, void *stream);
+/* Apply the neighbours' requests (ghost touched rows of rank-1 / rank+1, or
+ * NULL) to the owned boundary planes; *n_active = local |A_{it+2}|. */
+int eik_slab_apply_requests(const eik_geom *g, const uint32_t *req_lo, const uint32_t *req_hi, int64_t it,
+                            void *workspace, size_t workspace_bytes, int64_t *n_active, void *stream);
+/* Build pass on the owned planes: local #free and |R0|. */
+int eik_slab_build(const eik_geom *g, const double *phi, const double *speed, const uint8_t *state, double tol,
+                   void *workspace, size_t workspace_bytes, int64_t *free_cells, int64_t *flagged, void *stream);
+/* Remedy round `r` (0 uses R0); local |R_r| and |D_r|. */
+int eik_slab_remedy_round(const eik_geom *g, double *phi, const double *speed, const uint8_t *state, double tol,
+                          int64_t r, void *workspace, size_t workspace_bytes, int64_t *calls, int64_t *decs,
+                          void *stream);
 
 const char *eik_last_error(void);
 const char *eik_version(void);

@@ -30,7 +30,8 @@ NVCC_FLAGS = [
 EXPORTS = (
     "eik_workspace_size", "eik_ifim_update_step", "eik_build_remedy", "eik_remedy_load",
     "eik_remedy_export", "eik_remedy_step", "eik_ifim_solve", "eik_local_solve",
-    "eik_last_error", "eik_version",
+    "eik_last_error", "eik_version", "eik_workspace_offsets", "eik_slab_update_init", "eik_slab_update_iter",
+    "eik_slab_apply_requests", "eik_slab_build", "eik_slab_remedy_round",
 )
 
 
@@ -56,7 +57,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
 class Geom(C.Structure):
     _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64),
                 ("dx", C.c_double), ("dy", C.c_double), ("dz", C.c_double),
-                ("ndim", C.c_int32), ("dtype", C.c_int32)]
+                ("ndim", C.c_int32), ("dtype", C.c_int32), ("flags", C.c_int32), ("reserved", C.c_int32)]
+
+
+EIK_GEOM_SLAB = 1
 
 
 class Stats(C.Structure):
@@ -97,6 +101,12 @@ def lib():
     L.eik_remedy_step.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, SP, vp]
     L.eik_ifim_solve.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]
     L.eik_local_solve.argtypes = [C.c_int, P, P, P, P, dbl, dbl, P, i64, vp]
+    L.eik_workspace_offsets.argtypes = [GP, P]
+    L.eik_slab_update_init.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, C.POINTER(i64), vp]
+    L.eik_slab_update_iter.argtypes = [GP, P, P, P, dbl, i64, P, C.c_size_t, vp]
+    L.eik_slab_apply_requests.argtypes = [GP, P, P, i64, P, C.c_size_t, C.POINTER(i64), vp]
+    L.eik_slab_build.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, C.POINTER(i64), C.POINTER(i64), vp]
+    L.eik_slab_remedy_round.argtypes = [GP, P, P, P, dbl, i64, P, C.c_size_t, C.POINTER(i64), C.POINTER(i64), vp]
     L.eik_last_error.restype = C.c_char_p
     L.eik_version.restype = C.c_char_p
     _lib = L

@@ -69,6 +69,8 @@ struct Ctl {
     unsigned long long free_cells;  // build: #free
     unsigned long long flagged;     // build: |R0|
     unsigned long long dsum[3];     // remedy: |D_r| per rotating slot
+    unsigned long long nz_words;    // remedy diagnostics: non-empty member words / 4-cell sectors
+    unsigned long long nz_sectors;
 };
 
 // Division by a runtime-invariant divisor for dividends < 2^31 (round-up
@@ -100,6 +102,9 @@ struct KP {
     uint32_t nx32, plane32;  // cell indices are < 2^31 (make_layout)
     FastDiv fnx, fny, fW;
     double dx, dy, delta, tol;
+    int32_t slab;            // 1: z-slab of a sharded 3D grid, planes 0 and nz-1 are ghosts
+    int32_t pad1;
+    int64_t it0, max_it;     // iteration window of one persistent launch (slab mode: one step)
     double *P0, *P1;         // P0 = caller phi, P1 = workspace copy
     const double *F;         // speed
     double *dd;              // delta / F (uniform solvers)
@@ -430,6 +435,9 @@ __device__ __forceinline__ unsigned block_reserve(unsigned v, unsigned *glen, un
 // Preparation kernels
 // ---------------------------------------------------------------------------
 
+// Slab mode: ghost planes (neighbour ranks' boundary planes) are read, never computed.
+__device__ __forceinline__ bool ghost_plane(const KP &p, uint32_t z) { return p.slab && (z == 0 || z + 1 == (uint32_t)p.nz); }
+
 // apply_boundary writes (E/grid.py:212-215); validation is done by the caller.
 __global__ void k_seed(double *phi, uint8_t *state, const int64_t *idx, const double *val, int64_t n)
 {
@@ -460,8 +468,9 @@ __global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_
         const uint32_t blk = __ballot_sync(FULL, in && st == ST_BLOCKED);
         const uint32_t src = __ballot_sync(FULL, in && st == ST_SOURCE);
         if (lane == 0) {
-            p.Fb[w] = blk | src | ~q.rowm;  // lanes outside the row count as fixed
-            if (build_touched) p.Bt[w] = blk;
+            const bool gh = ghost_plane(p, q.z);
+            p.Fb[w] = gh ? FULL : (blk | src | ~q.rowm);  // lanes outside the row count as fixed
+            if (build_touched) p.Bt[w] = gh ? 0u : blk;   // ghost bits record activation requests
         }
     }
 }
@@ -488,6 +497,7 @@ __global__ void k_init_active(KP p, const int64_t *seeds, int64_t nseeds)
         }
         for (int t = 0; t < m; ++t) {
             const int64_t e = nb[t];
+            if (DIM == 3 && ghost_plane(p, (uint32_t)(e / p.plane))) continue;  // owned by a neighbour rank
             const uint8_t st = p.state[e];
             if (st == ST_BLOCKED || st == ST_SOURCE) continue;
             const int64_t row = e / p.nx;
@@ -518,15 +528,17 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
     __shared__ unsigned long long sred[WPB];
     Ctl *ctl = p.ctl;
     unsigned long long a_writes = 0, a_conv = 0;
-    const unsigned n0 = vload(&ctl->len[0]);
-    if (n0 == 0) return;  // no initial active cell: zero iterations
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        if (p.hist_cap > 0) p.hist[0] = (int64_t)n0;
-        ctl->sum = n0;
-        ctl->peak = n0;
+    if (!p.slab) {
+        const unsigned n0 = vload(&ctl->len[0]);
+        if (n0 == 0) return;  // no initial active cell: zero iterations
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            if (p.hist_cap > 0) p.hist[0] = (int64_t)n0;
+            ctl->sum = n0;
+            ctl->peak = n0;
+        }
     }
     const uint32_t nx = (uint32_t)p.nx, ny = (uint32_t)p.ny, nz = (uint32_t)p.nz;
-    for (int64_t it = 0;; ++it) {
+    for (int64_t it = p.it0; it < p.it0 + p.max_it; ++it) {
         const int par = (int)(it & 1);
         const double *__restrict__ Pc = par ? p.P1 : p.P0;
         double *__restrict__ Pn = par ? p.P0 : p.P1;
@@ -586,6 +598,8 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
                             const uint32_t re = k == 2 ? r - 1 : k == 3 ? r + 1 : k == 4 ? r - ny : k == 5 ? r + ny : r;
                             const uint32_t bit = 1u << (xe & 31);
                             old[k] = atomicOr(p.Bt + re * p.W + (xe >> 5), bit) | ~bit;
+                            // slab mode: a ghost-plane target is an activation request for its owner
+                            if (DIM == 3 && k >= 4 && ghost_plane(p, k == 4 ? z - 1 : z + 1)) old[k] = 0xffffffffu;
                         }
                     }
 #pragma unroll
@@ -607,6 +621,7 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
         }
         if (!grid_barrier(ctl)) return;
         const unsigned m = vload(&ctl->len[(it + 1) % 3]);
+        if (p.slab) continue;  // the host reduces the counts and decides
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             ctl->iters = it + 1;
             if (m) {
@@ -760,11 +775,18 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
                         du = z + 1 < p.nz ? __ldcg(Dp + w + planeW) : 0u;
                     }
                     const uint32_t dil = (c << 1) | (c >> 1) | (dw >> 31) | (de << 31) | ds | dn | dd | du;
-                    R[k] = c | (dil & ~__ldg(p.Fb + w));
-                    C[k] = c;
+                    const bool gh = DIM == 3 && ghost_plane(p, z);
+                    R[k] = gh ? 0u : (c | (dil & ~__ldg(p.Fb + w)));
+                    C[k] = gh ? 0u : c;
                 }
                 Dc[w] = 0;  // D_r is accumulated by phase A with atomicOr
                 cnt += __popc(R[k]);
+#ifdef EIK_DIAG
+                if (R[k]) {
+                    atomicAdd(&p.ctl->nz_words, 1ull);
+                    atomicAdd(&p.ctl->nz_sectors, (unsigned long long)__popc((R[k] | (R[k] >> 1) | (R[k] >> 2) | (R[k] >> 3)) & 0x11111111u));
+                }
+#endif
             }
         }
         unsigned pos = block_reserve(cnt, lenR, sscan);
@@ -798,16 +820,19 @@ __global__ void __launch_bounds__(BLOCK, 4) k_remedy(KP p, const unsigned *skip)
     if (skip && *skip) return;
     Ctl *ctl = p.ctl;
     const unsigned lane = lane_id();
-    const unsigned long long r0 = vload(&ctl->flagged);
-    if (r0 == 0) return;  // empty remedy set: zero rounds
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        ctl->peak = r0;
-        ctl->sum = 0;
+    if (!p.slab) {
+        const unsigned long long r0 = vload(&ctl->flagged);
+        if (r0 == 0) return;  // empty remedy set: zero rounds
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctl->peak = r0;
+            ctl->sum = 0;
+        }
     }
     const uint32_t nx = p.nx32, ny = (uint32_t)p.ny, nz = (uint32_t)p.nz;
     const uint32_t gt = blockIdx.x * BLOCK + threadIdx.x, GT = gridDim.x * BLOCK;
     uint32_t *ML = p.L0;
-    for (uint32_t r = 0;; ++r) {
+    for (int64_t rr = p.it0; rr < p.it0 + p.max_it; ++rr) {
+        const uint32_t r = (uint32_t)rr;
         const int par = (int)(r & 1);
         const double *__restrict__ Pc = par ? p.P1 : p.P0;
         double *__restrict__ Pn = par ? p.P0 : p.P1;
@@ -868,6 +893,7 @@ __global__ void __launch_bounds__(BLOCK, 4) k_remedy(KP p, const unsigned *skip)
                 wi = rw * p.W + (x >> 5);
                 bit = 1u << (x & 31);
             }
+#ifndef EIK_DBITS_RED
             // D_r bits: a warp's members of one word are contiguous in the list, so a
             // segmented OR-scan leaves each word's bits in its first lane, which
             // issues a single atomicOr for the word.
@@ -882,17 +908,54 @@ __global__ void __launch_bounds__(BLOCK, 4) k_remedy(KP p, const unsigned *skip)
             }
             const uint32_t pw = __shfl_up_sync(FULL, wi, 1);
             if (live && acc && (lane == 0 || pw != wi)) atomicOr(Dc + wi, acc);
+#else
+            // D_r bits: one fire-and-forget reduction per decreased member
+            if (dec) {
+                ++a_dec;
+                atomicOr(Dc + wi, bit);
+            }
+#endif
         }
+#ifndef EIK_DBITS_RED
         const unsigned long long td = block_sum(lane == 0 ? a_dec : 0ull, sred);
+#else
+        const unsigned long long td = block_sum(a_dec, sred);
+#endif
         if (threadIdx.x == 0 && td) atomicAdd(&ctl->dsum[r % 3], td);
         if (!grid_barrier(ctl)) return;
         const unsigned long long decs = vload(&ctl->dsum[r % 3]);
+        if (p.slab) continue;  // the host reduces the counts and decides
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->writes += decs;
         if (decs == 0) break;
         if (r + 1 >= (uint32_t)p.cap) {  // E/ifim.py:185-189
             if (blockIdx.x == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
             break;
         }
+    }
+}
+
+// Slab mode: activation requests from the neighbour ranks (their ghost-plane
+// touched words) for the owned boundary planes; a requested cell is activated
+// iff it is still FAR here (blocked cells are pre-touched).  The requester's
+// +inf test used the same snapshot value.  Appends to the next list of `it`.
+__global__ void k_apply_requests(KP p, const uint32_t *req_lo, const uint32_t *req_hi, int64_t it)
+{
+    const uint32_t planeW = (uint32_t)p.ny * p.W;
+    uint32_t *Ln = (it & 1) ? p.L0 : p.L1;
+    unsigned *lenN = &p.ctl->len[(it + 1) % 3];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < 2 * planeW; i += gridDim.x * blockDim.x) {
+        const bool hi = i >= planeW;
+        const uint32_t j = hi ? i - planeW : i;
+        const uint32_t *req = hi ? req_hi : req_lo;
+        if (!req) continue;
+        const uint32_t m = req[j];
+        if (!m) continue;
+        const uint32_t z = hi ? (uint32_t)p.nz - 2 : 1u;
+        const uint32_t w = z * planeW + j;
+        const uint32_t nb = m & ~atomicOr(p.Bt + w, m);
+        if (!nb) continue;
+        const uint32_t row = w / p.W, c0 = row * p.nx32 + (w - row * p.W) * 32u;
+        for (uint32_t b = nb; b; b &= b - 1) Ln[atomicAdd(lenN, 1u)] = c0 + (uint32_t)(__ffs(b) - 1);
     }
 }
 
@@ -951,6 +1014,8 @@ int make_layout(const eik_geom *g, Layout &L)
     if (g->ndim == 3 && !(g->dx == g->dy && g->dy == g->dz))
         return fail(EIK_EINVAL, "3D grids require dx == dy == dz (no anisotropic 3D solver, SPEC.md:169)");
     if (g->dtype != EIK_F64) return fail(EIK_EINVAL, "only float64 is supported");
+    if ((g->flags & EIK_GEOM_SLAB) && (g->ndim != 3 || g->nz < 3))
+        return fail(EIK_EINVAL, "a slab is 3D with at least one owned plane plus two ghost planes");
     L.N = g->nx * g->ny * g->nz;
     if (L.N >= (int64_t)1 << 31)
         return fail(EIK_EINVAL, "grid too large: %lld cells (limit 2^31 per device)", (long long)L.N);
@@ -999,6 +1064,9 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const doub
     p.fny = make_fastdiv((uint32_t)g->ny);
     p.fW = make_fastdiv(L.W);
     p.dx = g->dx; p.dy = g->dy; p.delta = g->dx; p.tol = tol;
+    p.slab = (g->flags & EIK_GEOM_SLAB) ? 1 : 0;
+    p.it0 = 0;
+    p.max_it = (int64_t)1 << 40;
     p.P0 = phi;
     p.P1 = (double *)(b + L.off_phi2);
     p.F = speed;
@@ -1437,10 +1505,155 @@ int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t 
     out->build_ms = ev.ms(1, 2);
     out->rem_ms = ev.ms(2, 3);
     out->total_ms = ev.ms(0, 3);
+    if (getenv("EIK_DIAG_PRINT"))
+        fprintf(stderr, "[eik diag] remedy member words %llu sectors %llu calls %llu\n",
+                (unsigned long long)c[1].nz_words, (unsigned long long)c[1].nz_sectors,
+                (unsigned long long)c[1].sum);
     if (history && history_cap > 0 && c[0].iters > 0) {
         const int64_t n = std::min<int64_t>((int64_t)c[0].iters, history_cap);
         CK(cudaMemcpy(history, b + L.off_hist, (size_t)n * 8, cudaMemcpyDeviceToHost));
     }
+    return EIK_OK;
+}
+
+int eik_workspace_offsets(const eik_geom *g, int64_t *off)
+{
+    Layout L;
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if (!off) return fail(EIK_EINVAL, "null output");
+    off[0] = (int64_t)L.off_phi2;
+    off[1] = (int64_t)L.off_bt;
+    off[2] = (int64_t)L.off_d0;
+    off[3] = (int64_t)L.off_d1;
+    return EIK_OK;
+}
+
+static int slab_check(const eik_geom *g, Layout &L, void *ws, size_t wsb)
+{
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if (!(g->flags & EIK_GEOM_SLAB)) return fail(EIK_EINVAL, "geometry is not a slab (flags)");
+    return check_ws(L, ws, wsb);
+}
+
+int eik_slab_update_init(const eik_geom *g, double *phi, const double *speed, uint8_t *state, const int64_t *seed_idx,
+                         const double *seed_val, int64_t nseeds, double tol, void *workspace, size_t workspace_bytes,
+                         int64_t *n_active, void *stream)
+{
+    Layout L;
+    int rc = slab_check(g, L, workspace, workspace_bytes);
+    if (rc) return rc;
+    if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
+    if (!phi || !speed || !state) return fail(EIK_EINVAL, "null array");
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t launches = 0;
+    rc = [&]() {
+        char *b = (char *)workspace;
+        Ctl *ctl = (Ctl *)(b + L.off_ctl_u);
+        CK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
+        if (nseeds > 0) {
+            k_seed<<<(int)std::min<int64_t>((nseeds + 255) / 256, 1024), 256, 0, st>>>(phi, state, seed_idx, seed_val,
+                                                                                       nseeds);
+            CK(cudaGetLastError());
+        }
+        KP p = make_kp(g, L, workspace, phi, speed, state, tol, ctl, L.cap_upd);
+        return dispatch(g, [&](auto E) {
+            int r2 = E.prep(p, true, true, st);
+            if (r2 || nseeds == 0) return r2;
+            return E.init_active(p, seed_idx, nseeds, st);
+        });
+    }();
+    (void)launches;
+    if (rc) return rc;
+    Ctl c;
+    CK(cudaMemcpyAsync(&c, (char *)workspace + L.off_ctl_u, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (n_active) *n_active = c.len[0];
+    return EIK_OK;
+}
+
+int eik_slab_update_iter(const eik_geom *g, double *phi, const double *speed, uint8_t *state, double tol, int64_t it,
+                         void *workspace, size_t workspace_bytes, void *stream)
+{
+    Layout L;
+    int rc = slab_check(g, L, workspace, workspace_bytes);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    Ctl *ctl = (Ctl *)((char *)workspace + L.off_ctl_u);
+    KP p = make_kp(g, L, workspace, phi, speed, state, tol, ctl, L.cap_upd);
+    p.it0 = it;
+    p.max_it = 1;
+    return dispatch(g, [&](auto E) { return E.update(p, st); });
+}
+
+int eik_slab_apply_requests(const eik_geom *g, const uint32_t *req_lo, const uint32_t *req_hi, int64_t it,
+                            void *workspace, size_t workspace_bytes, int64_t *n_active, void *stream)
+{
+    Layout L;
+    int rc = slab_check(g, L, workspace, workspace_bytes);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    Ctl *ctl = (Ctl *)((char *)workspace + L.off_ctl_u);
+    KP p = make_kp(g, L, workspace, nullptr, nullptr, nullptr, 1e-12, ctl, L.cap_upd);
+    const int64_t planeW = (int64_t)L.W * g->ny;
+    if (req_lo || req_hi) {
+        k_apply_requests<<<(int)std::min<int64_t>((2 * planeW + 255) / 256, 4096), 256, 0, st>>>(p, req_lo, req_hi, it);
+        CK(cudaGetLastError());
+    }
+    Ctl c;
+    CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if ((rc = check_hang(c, "slab update step"))) return rc;
+    if (n_active) *n_active = c.len[(it + 1) % 3];
+    return EIK_OK;
+}
+
+int eik_slab_build(const eik_geom *g, const double *phi, const double *speed, const uint8_t *state, double tol,
+                   void *workspace, size_t workspace_bytes, int64_t *free_cells, int64_t *flagged, void *stream)
+{
+    Layout L;
+    int rc = slab_check(g, L, workspace, workspace_bytes);
+    if (rc) return rc;
+    if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
+    cudaStream_t st = (cudaStream_t)stream;
+    Ctl *ctl = (Ctl *)((char *)workspace + L.off_ctl_r);
+    KP p = make_kp(g, L, workspace, const_cast<double *>(phi), speed, state, tol, ctl, L.cap_rem);
+    rc = dispatch(g, [&](auto E) { return E.build(p, phi, nullptr, st); });
+    if (rc) return rc;
+    Ctl c;
+    CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (free_cells) *free_cells = (int64_t)c.free_cells;
+    if (flagged) *flagged = (int64_t)c.flagged;
+    return EIK_OK;
+}
+
+int eik_slab_remedy_round(const eik_geom *g, double *phi, const double *speed, const uint8_t *state, double tol,
+                          int64_t r, void *workspace, size_t workspace_bytes, int64_t *calls, int64_t *decs,
+                          void *stream)
+{
+    Layout L;
+    int rc = slab_check(g, L, workspace, workspace_bytes);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    Ctl *ctl = (Ctl *)((char *)workspace + L.off_ctl_r);
+    KP p = make_kp(g, L, workspace, phi, speed, state, tol, ctl, L.cap_rem);
+    p.it0 = r;
+    p.max_it = 1;
+    if (r == 0) {  // round slots start clean (the build left R0 and its counters)
+        CK(cudaMemsetAsync(&ctl->len[0], 0, sizeof(ctl->len), st));
+        CK(cudaMemsetAsync(&ctl->cnt[0], 0, sizeof(ctl->cnt), st));
+        CK(cudaMemsetAsync(&ctl->dsum[0], 0, sizeof(ctl->dsum), st));
+    }
+    rc = dispatch(g, [&](auto E) { return E.remedy(p, nullptr, st); });
+    if (rc) return rc;
+    Ctl c;
+    CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if ((rc = check_hang(c, "slab remedy step"))) return rc;
+    if (calls) *calls = c.len[r % 3];
+    if (decs) *decs = (int64_t)c.dsum[r % 3];
     return EIK_OK;
 }
 

@@ -66,8 +66,8 @@ def _pick_device(grid) -> torch.device:
 def geometry(grid) -> _native.Geom:
     if getattr(grid, "ndim", 2) == 3:
         h = float(grid.h)
-        return _native.Geom(int(grid.nx), int(grid.ny), int(grid.nz), h, h, h, 3, 0)
-    return _native.Geom(int(grid.nx), int(grid.ny), 1, float(grid.dx), float(grid.dy), float(grid.dx), 2, 0)
+        return _native.Geom(int(grid.nx), int(grid.ny), int(grid.nz), h, h, h, 3, 0, 0, 0)
+    return _native.Geom(int(grid.nx), int(grid.ny), 1, float(grid.dx), float(grid.dy), float(grid.dx), 2, 0, 0, 0)
 
 
 class _DeviceGrid:
