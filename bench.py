@@ -14,8 +14,10 @@ SURVEY.md §8d).  `value` = total node updates / device time over all ranks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--size 512] [--impl ours|reference]
 
-N > 1 (torchrun): every rank solves its own full 512^3 instance (independent
-replicas, weak scaling); the time is the max over ranks.  --impl reference
+N > 1 (torchrun): ONE 512^3 grid is z-slab sharded over the ranks
+(paper_2106_15869_b200/slab.py: one ghost-plane / request / decrease-plane
+exchange per step over NCCL, counts all-reduced; strong scaling); the time is
+the max over ranks.  --slabs runs that protocol on one GPU.  --impl reference
 times the CPU oracle port of the reference algorithm (oracle/eik_oracle.c,
 OpenMP on all host cores) on a bounded sample of the same workload family.
 """
@@ -176,6 +178,59 @@ def run_reference(args):
     return 0
 
 
+class StepStats:
+    def __init__(self, calls, iterations, peak_remedy, rem_calls, rem_writes, rem_ms, launches, phase_ms):
+        self.calls, self.iterations, self.peak_remedy = calls, iterations, peak_remedy
+        self.rem_calls, self.rem_writes, self.rem_ms = rem_calls, rem_writes, rem_ms
+        self.launches, self.phase_ms = launches, phase_ms
+
+
+def make_single_step(eik, torch, dev, n, c, F):
+    """One device-resident solve_ifim of the whole grid (inputs restored in the step)."""
+    phi0 = torch.full((n, n, n), float("inf"), dtype=torch.float64, device=dev)
+    st0 = torch.zeros((n, n, n), dtype=torch.uint8, device=dev)
+    phi, st = torch.empty_like(phi0), torch.empty_like(st0)
+    g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), phi, F, st)
+    bc = eik.BoundaryCondition(((eik.CellIndex3D(c, c, c), 0.0),))
+
+    def step():
+        phi.copy_(phi0)
+        st.copy_(st0)
+        r = eik.solve_ifim(g, bc)
+        s = r.stats
+        ph = s.phases
+        rem_writes = s.phi_writes - (ph["update"]["solver_calls"] - ph["update"]["converged"])
+        return StepStats(s.solver_calls, s.iterations, s.peak_remedy, ph["remedy"]["solver_calls"], rem_writes,
+                         s.device_ms["remedy"], s.gpu_launches, {k: round(v, 3) for k, v in s.device_ms.items()})
+
+    return step
+
+
+def make_slab_step(torch, dev, n, c, F, world, rank):
+    """This rank's share of ONE z-sharded solve (paper_2106_15869_b200/slab.py protocol)."""
+    from paper_2106_15869_b200.slab import SlabPartition, SlabSolver, ThreadComm, TorchDistComm
+    from paper_2106_15869_b200.slab_gpu import SlabGpuEngine
+
+    comm = TorchDistComm() if world > 1 else ThreadComm(0, ThreadComm.make_shared(1))
+    z0, z1 = SlabPartition(n, world).bounds(rank)
+    st0 = torch.zeros((n, n, n), dtype=torch.uint8, device=dev)
+    e = SlabGpuEngine((n, n, n), 1.0, F, st0, z0, z1, dev)
+    clean_state = e.state.clone()
+    seeds = [((c * n + c) * n + c, 0.0)]
+    caps = (40 * 3 * n, 20 * 3 * n)
+
+    def step():
+        e.phi.fill_(float("inf"))
+        e.state.copy_(clean_state)
+        e.reset_counters()
+        ss = SlabSolver(e, comm, caps, tensor_device=dev).solve(seeds)
+        s = SlabSolver.combine(ss)
+        return StepStats(s.solver_calls, s.iterations, s.peak_remedy, e.rem_calls_local, e.rem_decs_local,
+                         e.rem_ms, e.launches, {"remedy_kernels_local": round(e.rem_ms, 3)})
+
+    return step
+
+
 def run_ours(args):
     import torch
 
@@ -194,28 +249,18 @@ def run_ours(args):
     blk = max(1, n // 16)
     c = n // 2
     workload = f"cfg4: 3D {n}^3 checkerboard 1:100 ({blk}^3 blocks), h=1, seed (c,c,c)"
-    # resident inputs
     kk = torch.arange(n, device=dev) // blk
     F = torch.where(((kk[:, None, None] + kk[None, :, None] + kk[None, None, :]) % 2) == 0, 1.0, 0.01).double()
-    phi0 = torch.full((n, n, n), float("inf"), dtype=torch.float64, device=dev)
-    st0 = torch.zeros((n, n, n), dtype=torch.uint8, device=dev)
-    phi = torch.empty_like(phi0)
-    st = torch.empty_like(st0)
-    g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), phi, F, st)
-    bc = eik.BoundaryCondition(((eik.CellIndex3D(c, c, c), 0.0),))
-
-    def step():
-        phi.copy_(phi0)
-        st.copy_(st0)
-        return eik.solve_ifim(g, bc)
+    slabs = world > 1 or args.slabs
+    step = make_slab_step(torch, dev, n, c, F, world, rank) if slabs else make_single_step(eik, torch, dev, n, c, F)
 
     for _ in range(args.warmup):
-        res = step()
+        r = step()
     torch.cuda.synchronize()
-    calls = res.stats.solver_calls
+    calls = r.calls
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    rem_ms = []
+    rem_ms, launches = [], 0
     if world > 1:
         import torch.distributed as dist
 
@@ -223,12 +268,11 @@ def run_ours(args):
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         e0.record(stream)
-        launches = 0
         for _ in range(args.steps):
             r = step()
-            rem_ms.append(r.stats.device_ms["remedy"])
-            launches += r.stats.gpu_launches
-            assert r.stats.solver_calls == calls
+            rem_ms.append(r.rem_ms)
+            launches += r.launches
+            assert r.calls == calls
         e1.record(stream)
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -239,38 +283,39 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
         dist.barrier()
-    value = calls * args.steps * world / (ms / 1e3)
+    # slabs: ONE grid sharded over all ranks (strong scaling)
+    value = calls * args.steps / (ms / 1e3)
     clocks = clk.summary()
 
-    # roofline of the dominant kernel (k_remedy): algorithmic bytes (SURVEY.md §8d:
-    # 8 B x (2 x solver_calls + phi_writes), remedy phase) / CUDA-event duration
-    ph = r.stats.phases
-    rem_calls = ph["remedy"]["solver_calls"]
-    rem_writes = r.stats.phi_writes - (ph["update"]["solver_calls"] - ph["update"]["converged"])
-    alg_bytes = 8.0 * (2 * rem_calls + rem_writes)
+    # roofline of the dominant kernel (k_remedy, this rank): algorithmic bytes (SURVEY.md §8d:
+    # 8 B x (2 x solver_calls + phi_writes) of the remedy phase) / its CUDA-event duration
+    alg_bytes = 8.0 * (2 * r.rem_calls + r.rem_writes)
     rem_s = statistics.median(rem_ms) / 1e3
     peak, peak_src = hbm_peak()
-    achieved = alg_bytes / rem_s / 1e9
-    traffic = traffic_from_profiles(workload)
+    achieved = alg_bytes / rem_s / 1e9 if rem_s > 0 else None
+    traffic = traffic_from_profiles(workload) if not slabs else None
 
     out = None
     if rank == 0:
-        # end to end through the public API with host (pinned) buffers
-        e2e = run_e2e(eik, torch, dev, n, blk, c, F.cpu().numpy(), calls, args)
+        e2e = run_e2e(eik, torch, dev, n, blk, c, F.cpu().numpy(), calls, args) if not slabs else \
+            {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+             "note": "e2e is measured by the single-GPU run through solve_ifim"}
         cpu_calls, cpu_s = cpu_sample(args.cpu_size, os.cpu_count() or 1) if not args.no_cpu else (0, 0.0)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "strong" if slabs else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload, "size": n, "solver_calls_per_step": calls,
-                       "iterations": r.stats.iterations, "peak_remedy": r.stats.peak_remedy,
-                       "parallelism": "replicas" if world > 1 else "single",
+                       "iterations": r.iterations, "peak_remedy": r.peak_remedy,
+                       "parallelism": f"z-slabs x{world} (host-driven exchange)" if slabs else "single",
                        "l2": "inputs larger than L2 (phi 1 GiB fp64 per field at 512^3)",
-                       "phase_ms": {k: round(v, 3) for k, v in r.stats.device_ms.items()}},
+                       "phase_ms": r.phase_ms},
             "wall_clock_to_convergence_ms": ms / args.steps,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": "k_remedy", "alg_bytes_per_launch": alg_bytes,
-                         "launch_ms": rem_s * 1e3, "peak_source": peak_src},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": "k_remedy", "alg_bytes_per_launch": alg_bytes, "launch_ms": rem_s * 1e3,
+                         "peak_source": peak_src},
             "cpu_baseline": {"value": (cpu_calls / cpu_s) if cpu_s else None, "unit": UNIT,
                              "cores": os.cpu_count() or 1, "kind": "port",
                              "sample": f"full solve of the {args.cpu_size}^3 checkerboard (same family) with "
@@ -323,6 +368,7 @@ def main():
     ap.add_argument("--cpu-size", type=int, default=96)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--slabs", action="store_true", help="use the z-slab protocol even on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -57,6 +57,13 @@ class SlabGpuEngine(SlabEngine):
         self.cur = 0  # phi buffer holding the current values
         self.it = 0
         self.r = 0
+        self.reset_counters()
+
+    def reset_counters(self):
+        """Local remedy counters + kernel time (bench roofline) and launch count."""
+        self.rem_calls_local = self.rem_decs_local = 0
+        self.rem_ms = 0.0
+        self.launches = 0
 
     @property
     def _stream(self):
@@ -87,12 +94,14 @@ class SlabGpuEngine(SlabEngine):
             C.byref(self.geom), _p(self.phi), _p(self.speed), _p(self.state), _p(si), _p(sv), len(idx), self.tol,
             self.ws.ptr, self.ws.nbytes, C.byref(n), self._stream))
         self.cur, self.it = 0, 0
+        self.launches += 4  # seeds, prep, initial activation (+ memsets)
         return int(n.value)
 
     def update_local(self):
         _native.check(_native.lib().eik_slab_update_iter(
             C.byref(self.geom), _p(self.phi), _p(self.speed), _p(self.state), self.tol, self.it, self.ws.ptr,
             self.ws.nbytes, self._stream))
+        self.launches += 2  # update iteration + request application
         self.it += 1
         self.cur = self.it & 1
         req_lo = self.touched[0].clone()
@@ -114,6 +123,7 @@ class SlabGpuEngine(SlabEngine):
             C.byref(self.geom), _p(self.phi), _p(self.speed), _p(self.state), self.tol, self.ws.ptr, self.ws.nbytes,
             C.byref(free), C.byref(flagged), self._stream))
         self.cur, self.r = 0, 0
+        self.launches += 2
         return int(free.value), int(flagged.value)
 
     def remedy_boundary_d(self):
@@ -129,9 +139,17 @@ class SlabGpuEngine(SlabEngine):
             Dp[0].copy_(g_lo) if g_lo is not None else Dp[0].zero_()
             Dp[self.nl + 1].copy_(g_hi) if g_hi is not None else Dp[self.nl + 1].zero_()
         calls, decs = C.c_int64(0), C.c_int64(0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         _native.check(_native.lib().eik_slab_remedy_round(
             C.byref(self.geom), _p(self.phi), _p(self.speed), _p(self.state), self.tol, self.r, self.ws.ptr,
             self.ws.nbytes, C.byref(calls), C.byref(decs), self._stream))
+        e1.record()
+        e1.synchronize()
+        self.rem_ms += e0.elapsed_time(e1)
+        self.rem_calls_local += int(calls.value)
+        self.rem_decs_local += int(decs.value)
+        self.launches += 1
         self.r += 1
         self.cur = self.r & 1
         return int(calls.value), int(decs.value)
