@@ -114,6 +114,17 @@ int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t 
 int eik_local_solve(int kind, const double *a, const double *b, const double *c, const double *f,
                     double dx, double dy, double *out, int64_t n, void *stream);
 
+/* solve_fixpoint (E/oracle.py:22-70): full-grid Jacobi passes, the independent
+ * ground truth; max_passes <= 0 selects the reference cap 10*(nx+ny[+nz]).
+ * out->iterations = passes, out->solver_calls = passes * free cells. */
+int eik_solve_fixpoint(const eik_geom *g, double *phi, const double *speed, uint8_t *state,
+                       const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
+                       int64_t max_passes, void *workspace, size_t workspace_bytes, eik_stats *out, void *stream);
+
+/* max_residual (E/harness.py:147-162): largest |phi - U(phi)| over free cells with finite phi. */
+int eik_max_residual(const eik_geom *g, const double *phi, const double *speed, const uint8_t *state,
+                     void *workspace, size_t workspace_bytes, double *out, void *stream);
+
 /* ---- z-slab sharding (protocol in paper_2106_15869_b200/slab.py) ----
  * The geometry is the rank's local slab with one ghost plane on each side
  * (flags = EIK_GEOM_SLAB, nz = owned planes + 2).  Every call runs one

@@ -31,7 +31,8 @@ EXPORTS = (
     "eik_workspace_size", "eik_ifim_update_step", "eik_build_remedy", "eik_remedy_load",
     "eik_remedy_export", "eik_remedy_step", "eik_ifim_solve", "eik_local_solve",
     "eik_last_error", "eik_version", "eik_workspace_offsets", "eik_slab_update_init", "eik_slab_update_iter",
-    "eik_slab_apply_requests", "eik_slab_build", "eik_slab_remedy_round",
+    "eik_slab_apply_requests", "eik_slab_build", "eik_slab_remedy_round", "eik_solve_fixpoint",
+    "eik_max_residual",
 )
 
 
@@ -107,6 +108,8 @@ def lib():
     L.eik_slab_apply_requests.argtypes = [GP, P, P, i64, P, C.c_size_t, C.POINTER(i64), vp]
     L.eik_slab_build.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, C.POINTER(i64), C.POINTER(i64), vp]
     L.eik_slab_remedy_round.argtypes = [GP, P, P, P, dbl, i64, P, C.c_size_t, C.POINTER(i64), C.POINTER(i64), vp]
+    L.eik_solve_fixpoint.argtypes = [GP, P, P, P, P, P, i64, dbl, i64, P, C.c_size_t, SP, vp]
+    L.eik_max_residual.argtypes = [GP, P, P, P, P, C.c_size_t, C.POINTER(dbl), vp]
     L.eik_last_error.restype = C.c_char_p
     L.eik_version.restype = C.c_char_p
     _lib = L

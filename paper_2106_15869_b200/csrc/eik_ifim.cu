@@ -40,6 +40,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "eik_ifim.h"
 
@@ -734,6 +735,9 @@ __global__ void k_remedy_export(KP p, uint8_t *member)
 // ---------------------------------------------------------------------------
 
 constexpr int REM_PER = 4;  // bitmap words per thread in phase B
+#ifndef REM_MU
+#define REM_MU 2            // phase A: members per lane in flight
+#endif
 
 
 template <int DIM>
@@ -812,8 +816,11 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
     }
 }
 
+#ifndef REM_MINB
+#define REM_MINB 4
+#endif
 template <int DIM, int SOL>
-__global__ void __launch_bounds__(BLOCK, 4) k_remedy(KP p, const unsigned *skip)
+__global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy(KP p, const unsigned *skip)
 {
     __shared__ unsigned sscan[WPB + 1];
     __shared__ unsigned long long sred[WPB];
@@ -853,74 +860,74 @@ __global__ void __launch_bounds__(BLOCK, 4) k_remedy(KP p, const unsigned *skip)
             ctl->sum += m;
             if (m > ctl->peak) ctl->peak = m;
         }
-        // ---- phase A: one local solve per member ----
+        // ---- phase A: one local solve per member, REM_MU members per lane in flight ----
         unsigned long long a_dec = 0;
-        uint32_t nxt = (gt < m) ? __ldcg(ML + gt) : 0u;
-        for (uint32_t i0 = gt - lane; i0 < m; i0 += GT) {
-            const uint32_t i = i0 + lane;
-            const bool live = i < m;
-            const uint32_t ent = nxt;
-            if (i + GT < m) nxt = __ldcg(ML + i + GT);  // prefetch the next member
-            bool dec = false;
-            uint32_t wi = 0, bit = 0;
-            if (live) {
-                const uint32_t c = ent & ~CARRY;
-                const uint32_t rw = fdiv(c, p.fnx);
-                const uint32_t x = c - rw * nx;
+        const uint32_t wbase = (gt - lane) * REM_MU, wstride = GT * REM_MU;
+        for (uint32_t i0 = wbase; i0 < m; i0 += wstride) {
+            uint32_t ent[REM_MU], rw[REM_MU], x[REM_MU];
+            bool live[REM_MU];
+            Sten s[REM_MU];
+#pragma unroll
+            for (int u = 0; u < REM_MU; ++u) {
+                const uint32_t i = i0 + u * 32 + lane;
+                live[u] = i < m;
+                ent[u] = live[u] ? __ldcg(ML + i) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < REM_MU; ++u) {
+                const uint32_t c = ent[u] & ~CARRY;
+                rw[u] = fdiv(c, p.fnx);
+                x[u] = c - rw[u] * nx;
                 uint32_t y, z = 0;
                 if (DIM == 3) {
-                    z = fdiv(rw, p.fny);
-                    y = rw - z * ny;
+                    z = fdiv(rw[u], p.fny);
+                    y = rw[u] - z * ny;
                 } else {
-                    y = rw;
+                    y = rw[u];
                 }
-                Sten s;
-                s.c = __ldca(Pc + c);
-                s.w = x > 0 ? __ldca(Pc + (c - 1)) : INFINITY;
-                s.e = x + 1 < nx ? __ldca(Pc + (c + 1)) : INFINITY;
-                s.s = y > 0 ? __ldca(Pc + (c - nx)) : INFINITY;
-                s.n = y + 1 < ny ? __ldca(Pc + (c + nx)) : INFINITY;
-                s.d = s.u = INFINITY;
-                if (DIM == 3) {
-                    s.d = z > 0 ? __ldca(Pc + (c - p.plane32)) : INFINITY;
-                    s.u = z + 1 < nz ? __ldca(Pc + (c + p.plane32)) : INFINITY;
+                Sten &t = s[u];
+                t.c = t.w = t.e = t.s = t.n = t.d = t.u = INFINITY;
+                t.k = 1.0;
+                if (live[u]) {
+                    t.c = __ldca(Pc + c);
+                    if (x[u] > 0) t.w = __ldca(Pc + (c - 1));
+                    if (x[u] + 1 < nx) t.e = __ldca(Pc + (c + 1));
+                    if (y > 0) t.s = __ldca(Pc + (c - nx));
+                    if (y + 1 < ny) t.n = __ldca(Pc + (c + nx));
+                    if (DIM == 3) {
+                        if (z > 0) t.d = __ldca(Pc + (c - p.plane32));
+                        if (z + 1 < nz) t.u = __ldca(Pc + (c + p.plane32));
+                    }
+                    t.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
                 }
-                s.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
-                const double v = solve<DIM, SOL>(p, s);
-                dec = v < s.c - p.tol;  // E/ifim.py:203
-                if (dec) Pn[c] = v;
-                else if (ent & CARRY) Pn[c] = s.c;  // changed last round: carry into the other buffer
-                wi = rw * p.W + (x >> 5);
-                bit = 1u << (x & 31);
             }
-#ifndef EIK_DBITS_RED
-            // D_r bits: a warp's members of one word are contiguous in the list, so a
-            // segmented OR-scan leaves each word's bits in its first lane, which
-            // issues a single atomicOr for the word.
-            a_dec += __popc(__ballot_sync(FULL, dec));
-            if (!live) wi = 0xffffffffu;
-            uint32_t acc = dec ? bit : 0u;
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t ov = __shfl_down_sync(FULL, acc, o);
-                const uint32_t ow = __shfl_down_sync(FULL, wi, o);
-                if (lane + o < 32 && ow == wi) acc |= ov;
+            for (int u = 0; u < REM_MU; ++u) {
+                const uint32_t c = ent[u] & ~CARRY;
+                bool dec = false;
+                if (live[u]) {
+                    const double v = solve<DIM, SOL>(p, s[u]);
+                    dec = v < s[u].c - p.tol;  // E/ifim.py:203
+                    if (dec) Pn[c] = v;
+                    else if (ent[u] & CARRY) Pn[c] = s[u].c;  // changed last round: carry into the other buffer
+                }
+                // D_r bits: a warp's members of one word are contiguous in the list, so a
+                // segmented OR-scan leaves each word's bits in its first lane, which
+                // issues a single atomicOr for the word.
+                a_dec += __popc(__ballot_sync(FULL, dec));
+                const uint32_t wi = live[u] ? rw[u] * p.W + (x[u] >> 5) : 0xffffffffu;
+                uint32_t acc = dec ? (1u << (x[u] & 31)) : 0u;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t ov = __shfl_down_sync(FULL, acc, o);
+                    const uint32_t ow = __shfl_down_sync(FULL, wi, o);
+                    if (lane + o < 32 && ow == wi) acc |= ov;
+                }
+                const uint32_t pw = __shfl_up_sync(FULL, wi, 1);
+                if (live[u] && acc && (lane == 0 || pw != wi)) atomicOr(Dc + wi, acc);
             }
-            const uint32_t pw = __shfl_up_sync(FULL, wi, 1);
-            if (live && acc && (lane == 0 || pw != wi)) atomicOr(Dc + wi, acc);
-#else
-            // D_r bits: one fire-and-forget reduction per decreased member
-            if (dec) {
-                ++a_dec;
-                atomicOr(Dc + wi, bit);
-            }
-#endif
         }
-#ifndef EIK_DBITS_RED
         const unsigned long long td = block_sum(lane == 0 ? a_dec : 0ull, sred);
-#else
-        const unsigned long long td = block_sum(a_dec, sred);
-#endif
         if (threadIdx.x == 0 && td) atomicAdd(&ctl->dsum[r % 3], td);
         if (!grid_barrier(ctl)) return;
         const unsigned long long decs = vload(&ctl->dsum[r % 3]);
@@ -932,6 +939,105 @@ __global__ void __launch_bounds__(BLOCK, 4) k_remedy(KP p, const unsigned *skip)
             break;
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Fixpoint reference (E/oracle.py:22-70): full-grid Jacobi passes
+// phi <- min(phi, U(snapshot)) over every free cell until nothing decreases or
+// the largest decrease is below tol; cap 10*(nx+ny[+nz]) passes.  Every free
+// cell writes the other buffer each pass, so the double buffer stays exact.
+// max_change is reduced with atomicMax on the IEEE bits (non-negative doubles
+// order like their bit patterns; +inf for first reaches).
+// ---------------------------------------------------------------------------
+
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK) k_fixpoint(KP p)
+{
+    __shared__ unsigned long long sred[WPB];
+    Ctl *ctl = p.ctl;
+    const unsigned lane = lane_id();
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
+    for (int64_t it = 0;; ++it) {
+        const int par = (int)(it & 1);
+        const double *__restrict__ Pc = par ? p.P1 : p.P0;
+        double *__restrict__ Pn = par ? p.P0 : p.P1;
+        unsigned long long a_dec = 0, a_max = 0;
+        for (uint32_t w = gw; w < p.nwords; w += GW) {
+            const WPos q = wpos<DIM>(p, w);
+            const uint32_t freem = q.rowm & ~__ldg(p.Fb + w);
+            if (freem == 0) continue;
+            Sten s;
+            gather<DIM, SOL>(p, Pc, q, freem, s);
+            bool dec = false;
+            if ((freem >> lane) & 1u) {
+                const double cand = solve<DIM, SOL>(p, s);
+                const double nw = dmin(s.c, cand);  // np.minimum(old, candidates)
+                dec = nw < s.c;
+                if (dec) {
+                    const double ch = s.c - nw;
+                    const unsigned long long b = (unsigned long long)__double_as_longlong(ch);
+                    if (b > a_max) a_max = b;
+                }
+                Pn[q.c0 + lane] = nw;
+            }
+            const uint32_t bm = __ballot_sync(FULL, dec);
+            if (lane == 0) a_dec += __popc(bm);
+        }
+        unsigned long long m = a_max;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long t = __shfl_xor_sync(FULL, m, o);
+            m = t > m ? t : m;
+        }
+        const unsigned long long td = block_sum(a_dec, sred);
+        if (lane == 0 && m) atomicMax(&ctl->cnt[(it % 3)], m);  // cnt[] slots hold max-change bits here
+        if (threadIdx.x == 0) {
+            if (td) atomicAdd(&ctl->dsum[it % 3], td);
+            if (blockIdx.x == 0) {
+                ctl->cnt[(it + 1) % 3] = 0;
+                ctl->dsum[(it + 1) % 3] = 0;
+            }
+        }
+        if (!grid_barrier(ctl)) return;
+        const unsigned long long decs = vload(&ctl->dsum[it % 3]);
+        const double maxch = __longlong_as_double((long long)vload(&ctl->cnt[it % 3]));
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->iters = it + 1;
+        if (decs == 0 || maxch < p.tol) break;  // E/oracle.py:59-62
+        if (it + 1 >= p.cap) {                   // E/oracle.py:63-67
+            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
+            break;
+        }
+    }
+}
+
+// max_residual (E/harness.py:147-162): max |phi - U(phi)| over free cells with
+// finite phi; result as IEEE bits in ctl->peak.
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK) k_residual(KP p)
+{
+    const unsigned lane = lane_id();
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
+    unsigned long long a_max = 0;
+    for (uint32_t w = gw; w < p.nwords; w += GW) {
+        const WPos q = wpos<DIM>(p, w);
+        const uint32_t freem = q.rowm & ~__ldg(p.Fb + w);
+        if (freem == 0) continue;
+        Sten s;
+        gather<DIM, SOL>(p, p.P0, q, freem, s);
+        if (((freem >> lane) & 1u) && s.c < INFINITY) {
+            const double r = fabs(s.c - solve<DIM, SOL>(p, s));
+            const unsigned long long b = (unsigned long long)__double_as_longlong(r);
+            if (r == r && b > a_max) a_max = b;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(FULL, a_max, o);
+        a_max = t > a_max ? t : a_max;
+    }
+    if (lane == 0 && a_max) atomicMax(&p.ctl->peak, a_max);
 }
 
 // Slab mode: activation requests from the neighbour ranks (their ghost-plane
@@ -1109,12 +1215,14 @@ int stream_grid(int64_t work_warps)
 }
 
 template <typename K>
-int coop_launch(K kernel, KP &p, const unsigned *skip, bool with_skip, cudaStream_t st)
+int coop_launch(K kernel, KP &p, const unsigned *skip, bool with_skip, cudaStream_t st, const char *env_name,
+                int default_per_sm)
 {
     int per_sm = 0;
     cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, BLOCK, 0);
     if (e != cudaSuccess) return fail(EIK_ECUDA, "occupancy: %s", cudaGetErrorString(e));
-    if (const char *env = getenv("EIK_BLOCKS_PER_SM")) {
+    if (default_per_sm > 0 && default_per_sm < per_sm) per_sm = default_per_sm;
+    if (const char *env = getenv(env_name)) {  // tuning override
         const int v = atoi(env);
         if (v > 0 && v < per_sm) per_sm = v;
     }
@@ -1145,7 +1253,10 @@ struct Engine {
         CK(cudaGetLastError());
         return EIK_OK;
     }
-    static int update(KP &p, cudaStream_t st) { return coop_launch(k_update<DIM, SOL>, p, nullptr, false, st); }
+    static int update(KP &p, cudaStream_t st)
+    {
+        return coop_launch(k_update<DIM, SOL>, p, nullptr, false, st, "EIK_UPD_BLOCKS_PER_SM", 0);
+    }
     // remedy-set slots: counters (R0 is rewritten word by word)
     static int reset_set(KP &p, cudaStream_t st)
     {
@@ -1174,9 +1285,19 @@ struct Engine {
         CK(cudaGetLastError());
         return EIK_OK;
     }
+    static int fixpoint(KP &p, cudaStream_t st)
+    {
+        return coop_launch(k_fixpoint<DIM, SOL>, p, nullptr, false, st, "EIK_FIX_BLOCKS_PER_SM", 0);
+    }
+    static int residual(KP &p, cudaStream_t st)
+    {
+        k_residual<DIM, SOL><<<stream_grid(p.nwords), BLOCK, 0, st>>>(p);
+        CK(cudaGetLastError());
+        return EIK_OK;
+    }
     static int remedy(KP &p, const unsigned *skip, cudaStream_t st)
     {
-        return coop_launch(k_remedy<DIM, SOL>, p, skip, true, st);
+        return coop_launch(k_remedy<DIM, SOL>, p, skip, true, st, "EIK_REM_BLOCKS_PER_SM", 0);
     }
 };
 
@@ -1516,6 +1637,89 @@ int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t 
     return EIK_OK;
 }
 
+int eik_solve_fixpoint(const eik_geom *g, double *phi, const double *speed, uint8_t *state,
+                       const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
+                       int64_t max_passes, void *workspace, size_t workspace_bytes, eik_stats *out, void *stream)
+{
+    Layout L;
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if ((rc = check_ws(L, workspace, workspace_bytes))) return rc;
+    if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
+    if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
+    if (nseeds < 1 || !seed_idx || !seed_val) return fail(EIK_EINVAL, "boundary condition has no seeds");
+    cudaStream_t st = (cudaStream_t)stream;
+    memset(out, 0, sizeof(*out));
+    char *b = (char *)workspace;
+    Ctl *ctl = (Ctl *)(b + L.off_ctl_r);
+    const int64_t s3 = g->nx + g->ny + (g->ndim == 3 ? g->nz : 0);
+    const int64_t cap = max_passes > 0 ? max_passes : 10 * s3;  // E/oracle.py:40
+    Events ev;
+    ev.rec(0, st);
+    CK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
+    k_seed<<<(int)std::min<int64_t>((nseeds + 255) / 256, 1024), 256, 0, st>>>(phi, state, seed_idx, seed_val, nseeds);
+    CK(cudaGetLastError());
+    KP p = make_kp(g, L, workspace, phi, speed, state, tol, ctl, cap);
+    rc = dispatch(g, [&](auto E) {
+        int r = E.prep(p, true, false, st);
+        if (r) return r;
+        return E.fixpoint(p, st);
+    });
+    if (rc) return rc;
+    ev.rec(1, st);
+    Ctl c;
+    CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if ((rc = check_hang(c, "fixpoint"))) return rc;
+    if (c.iters & 1) {  // the last pass wrote the workspace buffer
+        CK(cudaMemcpyAsync(phi, p.P1, (size_t)L.N * 8, cudaMemcpyDeviceToDevice, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    int64_t nfree = 0;
+    {
+        // free cells = N - #(blocked | source): count from the fixed bitmap
+        std::vector<uint32_t> fb(L.nwords);
+        CK(cudaMemcpy(fb.data(), p.Fb, (size_t)L.nwords * 4, cudaMemcpyDeviceToHost));
+        int64_t fixed_in_row = 0;
+        for (uint32_t w = 0; w < L.nwords; ++w) fixed_in_row += __builtin_popcount(fb[w]);
+        nfree = (int64_t)L.nwords * 32 - fixed_in_row;  // lanes outside rows are marked fixed
+    }
+    out->iterations = (int64_t)c.iters;
+    out->solver_calls = (int64_t)c.iters * nfree;  // E/oracle.py:52
+    out->total_ms = ev.ms(0, 1);
+    out->gpu_launches = 3;
+    if (c.err == EIK_ECAP) return fail(EIK_ECAP, "fixpoint iteration did not converge within %lld passes", (long long)cap);
+    return EIK_OK;
+}
+
+int eik_max_residual(const eik_geom *g, const double *phi, const double *speed, const uint8_t *state,
+                     void *workspace, size_t workspace_bytes, double *out, void *stream)
+{
+    Layout L;
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if ((rc = check_ws(L, workspace, workspace_bytes))) return rc;
+    if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
+    cudaStream_t st = (cudaStream_t)stream;
+    Ctl *ctl = (Ctl *)((char *)workspace + L.off_ctl_r);
+    CK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
+    KP p = make_kp(g, L, workspace, const_cast<double *>(phi), speed, state, 1e-12, ctl, 0);
+    rc = dispatch(g, [&](auto E) {
+        int r = E.prep(p, false, false, st);
+        if (r) return r;
+        return E.residual(p, st);
+    });
+    if (rc) return rc;
+    Ctl c;
+    CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    unsigned long long bits = c.peak;
+    double r;
+    memcpy(&r, &bits, 8);
+    *out = r;  // 0.0 when no free finite cell (E/harness.py:158-159)
+    return EIK_OK;
+}
+
 int eik_workspace_offsets(const eik_geom *g, int64_t *off)
 {
     Layout L;
@@ -1547,7 +1751,6 @@ int eik_slab_update_init(const eik_geom *g, double *phi, const double *speed, ui
     if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
     if (!phi || !speed || !state) return fail(EIK_EINVAL, "null array");
     cudaStream_t st = (cudaStream_t)stream;
-    int64_t launches = 0;
     rc = [&]() {
         char *b = (char *)workspace;
         Ctl *ctl = (Ctl *)(b + L.off_ctl_u);
@@ -1564,7 +1767,6 @@ int eik_slab_update_init(const eik_geom *g, double *phi, const double *speed, ui
             return E.init_active(p, seed_idx, nseeds, st);
         });
     }();
-    (void)launches;
     if (rc) return rc;
     Ctl c;
     CK(cudaMemcpyAsync(&c, (char *)workspace + L.off_ctl_u, sizeof(Ctl), cudaMemcpyDeviceToHost, st));

@@ -1,9 +1,9 @@
 """Dispatch and parity helpers for the iFIM path (E/harness.py:54-57, 121-179).
 
 ``run_method`` keeps the reference's string dispatch (the plugin point every
-CLI command goes through, E/harness.py:121-144).  Only "ifim" is served by
-this package; the other reference methods (fmm, fsm, fim, oracle) are out of
-scope and raise like an unknown method would.
+CLI command goes through, E/harness.py:121-144).  "ifim" and "oracle" (the
+fixpoint ground truth, E/oracle.py) are served by this package; fmm, fsm and
+fim are out of scope and raise like an unknown method would.
 """
 from __future__ import annotations
 
@@ -12,17 +12,20 @@ import hashlib
 import numpy as np
 import torch
 
+from .fixpoint import max_residual, solve_fixpoint  # noqa: F401  (re-exported)
 from .ifim import solve_ifim
 from .result import SolverResult
 
-METHOD_NAMES = ("ifim",)
-PARALLEL_METHODS = frozenset({"ifim"})
+METHOD_NAMES = ("ifim", "oracle")
+PARALLEL_METHODS = frozenset({"ifim", "oracle"})
 
 
 def run_method(method: str, grid, bc, tol: float = 1e-12, workers: int = 1) -> SolverResult:
     """E/harness.py:121-144 restricted to the accelerated method."""
     if method == "ifim":
         return solve_ifim(grid, bc, tol=tol, workers=workers)
+    if method == "oracle":
+        return solve_fixpoint(grid, bc, tol=tol, workers=workers)
     raise ValueError(f"unknown method {method!r}, expected one of {METHOD_NAMES}")
 
 

@@ -1,0 +1,107 @@
+"""GPU fixpoint / residual vs the CPU restatement and the
+reference's own fixpoint output, plus full-size properties of the iFIM field."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2106_15869_b200 as eik
+from oracle import cpu
+
+pytestmark = pytest.mark.gpu
+
+
+def test_fixpoint_matches_reference_golden(staged2d):
+    """ex1 32^2 fixpoint produced by the live reference (E/oracle.py)."""
+    Z = staged2d
+    ny, nx = Z["stale_phi_in"].shape
+    dx = float(Z["stale_dx"][0])
+    g = eik.Grid(nx, ny, dx, dx, (-10.0, -10.0), np.full((ny, nx), np.inf), Z["stale_speed"].copy(),
+                 np.where(Z["stale_speed"] == 0, 4, 0).astype(np.uint8))
+    src = np.flatnonzero(Z["stale_state"].ravel() == eik.CellState.SOURCE)
+    vals = Z["stale_fixpoint"].ravel()[src]
+    bc = eik.BoundaryCondition(tuple((eik.CellIndex(int(c % nx), int(c // nx)), float(v)) for c, v in zip(src, vals)))
+    res = eik.solve_fixpoint(g, bc)
+    assert np.array_equal(res.phi.view(np.uint64), Z["stale_fixpoint"].view(np.uint64))
+
+
+@pytest.mark.parametrize("kind", ["2d", "aniso", "3d"])
+def test_fixpoint_bit_exact_vs_oracle(cases2d, cases3d, kind):
+    if kind == "3d":
+        meta, Z = cases3d
+        names = list(meta)
+    else:
+        meta, Z = cases2d
+        names = ["aniso_53x37", "sealed_40x20"] if kind == "aniso" else ["ex2_48", "ex5_48", "pocket_24", "checker_64"]
+    for name in names:
+        m = meta[name]
+        if kind == "3d":
+            shape, sp = (m["nz"], m["ny"], m["nx"]), m["h"]
+            g = eik.new_grid_3d(m["nx"], m["ny"], m["nz"], m["h"], speed=Z[name + "__speed"].reshape(shape))
+            cells = [eik.CellIndex3D(c % m["nx"], (c // m["nx"]) % m["ny"], c // (m["nx"] * m["ny"]))
+                     for c in Z[name + "__seed_idx"].tolist()]
+        else:
+            shape, sp = (m["ny"], m["nx"]), (m["dx"], m["dy"])
+            g = eik.new_grid(m["nx"], m["ny"], m["dx"], m["dy"], speed=Z[name + "__speed"])
+            cells = [eik.CellIndex(c % m["nx"], c // m["nx"]) for c in Z[name + "__seed_idx"].tolist()]
+        bc = eik.BoundaryCondition(tuple(zip(cells, Z[name + "__seed_val"].tolist())))
+        res = eik.solve_fixpoint(g, bc)
+        ref, st = cpu.solve_fixpoint(shape, sp, Z[name + "__speed"], Z[name + "__seed_idx"], Z[name + "__seed_val"])
+        assert np.array_equal(res.phi.view(np.uint64), ref.view(np.uint64)), name
+        assert (res.stats.iterations, res.stats.solver_calls) == (st["iterations"], st["solver_calls"]), name
+        assert eik.max_residual(g) <= 1e-9
+
+
+def test_max_residual_flags_a_stale_cell():
+    g = eik.new_grid(32, 32, 1.0, 1.0)
+    eik.solve_ifim(g, eik.seed_point(g, (3, 4), 0.0))
+    assert eik.max_residual(g) <= 1e-12
+    g.phi[20, 14] += 0.3
+    assert abs(eik.max_residual(g) - 0.3) < 1e-9
+
+
+@pytest.mark.slow
+def test_full_size_ifim_equals_fixpoint_256():
+    """cfg3-like: 3D 256^3, F=1, 16 random seeds -- iFIM vs the independent fixpoint
+    (T/test_ifim.py:23-30 agreement <= 1e-9) and the residual gate."""
+    n = 256
+    rng = np.random.default_rng(2106)
+    seeds = set()
+    while len(seeds) < 16:
+        seeds.add(tuple(int(v) for v in rng.integers(0, n, 3)))
+    bc = eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in sorted(seeds)))
+    dev = torch.device("cuda:0")
+
+    def grid():
+        return eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), np.inf, dtype=torch.float64, device=dev),
+                          torch.ones((n, n, n), dtype=torch.float64, device=dev),
+                          torch.zeros((n, n, n), dtype=torch.uint8, device=dev))
+
+    g1, g2 = grid(), grid()
+    r1 = eik.solve_ifim(g1, bc)
+    r2 = eik.solve_fixpoint(g2, bc)
+    assert torch.max(torch.abs(r1.phi - r2.phi)).item() <= 1e-9
+    assert eik.max_residual(g1) <= 1e-9
+    # exact-distance check: first-order error bounded like the 2D calibration (~0.3 h ln n per axis)
+    z, y, x = torch.meshgrid(*(torch.arange(n, device=dev, dtype=torch.float64),) * 3, indexing="ij")
+    exact = torch.full_like(r1.phi, np.inf)
+    for s in seeds:
+        exact = torch.minimum(exact, torch.sqrt((x - s[0]) ** 2 + (y - s[1]) ** 2 + (z - s[2]) ** 2))
+    err = (r1.phi - exact).abs()
+    assert err.max().item() <= 0.6 * np.log(n)  # first-order scheme: error ~ C h ln n (SURVEY.md §7 hard part 6)
+
+
+def test_exact_distance_error_equals_oracle_64():
+    """Constant-speed check against the exact distance: the GPU field's error equals
+    the CPU oracle's error (SURVEY.md §8c/BASELINE.md parity gate)."""
+    n = 64
+    rng = np.random.default_rng(7)
+    seeds = sorted({tuple(int(v) for v in rng.integers(0, n, 3)) for _ in range(16)})
+    g = eik.new_grid_3d(n, n, n, 1.0)
+    res = eik.solve_ifim(g, eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in seeds)))
+    lin = [(k * n + j) * n + i for i, j, k in seeds]
+    ref = cpu.solve_ifim((n, n, n), 1.0, np.ones((n, n, n)), lin, [0.0] * len(lin), threads=8)
+    z, y, x = np.meshgrid(*(np.arange(n, dtype=np.float64),) * 3, indexing="ij")
+    exact = np.min([np.sqrt((x - i) ** 2 + (y - j) ** 2 + (z - k) ** 2) for i, j, k in seeds], axis=0)
+    e_gpu, e_cpu = np.abs(res.phi - exact), np.abs(ref.phi - exact)
+    assert np.max(np.abs(e_gpu - e_cpu)) <= 1e-10
+    assert e_gpu.max() <= 0.6 * np.log(n)
