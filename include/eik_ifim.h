@@ -156,6 +156,29 @@ int eik_slab_remedy_round(const eik_geom *g, double *phi, const double *speed, c
                           int64_t r, void *workspace, size_t workspace_bytes, int64_t *calls, int64_t *decs,
                           void *stream);
 
+/* ---- multi-rank peer slabs (B200 path: no host round trips) ----
+ * One z-sharded 3D grid over R ranks.  Each rank owns consecutive planes and
+ * keeps them in its own phi buffer + workspace; the persistent kernels read the
+ * neighbours' boundary planes / decrease rows and activate cells on them
+ * through device-visible pointers (NVLink peer mappings on a multi-GPU box, or
+ * plain device pointers when R ranks are emulated on one GPU), with a
+ * hierarchical grid + cross-rank barrier per iteration.  ranks[] describes all
+ * R ranks as seen from this process; this process runs ranks [r_begin, r_end)
+ * and passes their speed/state arrays.  Seeds are global linear indices.
+ * Multi-process use needs a host barrier between eik_mr_prepare and eik_mr_run
+ * on every rank.  Stats are global (identical on every rank). */
+typedef struct eik_rank {
+    double *phi0;    /* the rank's phi (owned planes), result buffer */
+    void *workspace; /* the rank's workspace (eik_workspace_size of its local slab geometry) */
+    int64_t nz;      /* owned planes */
+} eik_rank;
+int eik_mr_prepare(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_begin, int32_t r_end,
+                   const double *const *speed, uint8_t *const *state, const int64_t *seeds, const double *seed_val,
+                   int64_t nseeds, double tol, void *stream);
+int eik_mr_run(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_begin, int32_t r_end,
+               const double *const *speed, uint8_t *const *state, double tol, int64_t *history, int64_t history_cap,
+               eik_stats *out, void *stream);
+
 const char *eik_last_error(void);
 const char *eik_version(void);
 

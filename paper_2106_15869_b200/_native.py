@@ -32,7 +32,7 @@ EXPORTS = (
     "eik_remedy_export", "eik_remedy_step", "eik_ifim_solve", "eik_local_solve",
     "eik_last_error", "eik_version", "eik_workspace_offsets", "eik_slab_update_init", "eik_slab_update_iter",
     "eik_slab_apply_requests", "eik_slab_build", "eik_slab_remedy_round", "eik_solve_fixpoint",
-    "eik_max_residual",
+    "eik_max_residual", "eik_mr_prepare", "eik_mr_run",
 )
 
 
@@ -62,6 +62,10 @@ class Geom(C.Structure):
 
 
 EIK_GEOM_SLAB = 1
+
+
+class Rank(C.Structure):
+    _fields_ = [("phi0", C.c_void_p), ("workspace", C.c_void_p), ("nz", C.c_int64)]
 
 
 class Stats(C.Structure):
@@ -110,6 +114,9 @@ def lib():
     L.eik_slab_remedy_round.argtypes = [GP, P, P, P, dbl, i64, P, C.c_size_t, C.POINTER(i64), C.POINTER(i64), vp]
     L.eik_solve_fixpoint.argtypes = [GP, P, P, P, P, P, i64, dbl, i64, P, C.c_size_t, SP, vp]
     L.eik_max_residual.argtypes = [GP, P, P, P, P, C.c_size_t, C.POINTER(dbl), vp]
+    RP = C.POINTER(Rank)
+    L.eik_mr_prepare.argtypes = [GP, C.c_int32, RP, C.c_int32, C.c_int32, P, P, P, P, i64, dbl, vp]
+    L.eik_mr_run.argtypes = [GP, C.c_int32, RP, C.c_int32, C.c_int32, P, P, dbl, P, i64, SP, vp]
     L.eik_last_error.restype = C.c_char_p
     L.eik_version.restype = C.c_char_p
     _lib = L

@@ -38,6 +38,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
+#include <cstddef>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -72,6 +73,22 @@ struct Ctl {
     unsigned long long dsum[3];     // remedy: |D_r| per rotating slot
     unsigned long long nz_words;    // remedy diagnostics: non-empty member words / 4-cell sectors
     unsigned long long nz_sectors;
+    unsigned wcount;                // multi-rank: world-barrier arrivals (rank 0's copy is used)
+    unsigned wgen;                  // multi-rank: this rank's world-barrier generation
+};
+
+constexpr int EIK_MAX_RANKS = 16;
+
+// A neighbour rank's buffers, addressable from this device (same GPU, or an
+// NVLink peer mapping).  Multi-rank (peer-slab) mode reads its boundary planes
+// of phi and of the decrease bitmap directly and activates cells on its
+// boundary plane with atomics on its touched bitmap and next worklist.
+struct Peer {
+    double *P0, *P1;
+    uint32_t *Bt, *L0, *L1, *D0b, *D1b;
+    Ctl *ctl;
+    uint32_t nz;     // its owned planes
+    uint32_t valid;
 };
 
 // Division by a runtime-invariant divisor for dividends < 2^31 (round-up
@@ -101,6 +118,7 @@ struct KP {
     int64_t nx, ny, nz, plane;
     uint32_t W, nwords, nrows, pad0;
     uint32_t nx32, plane32;  // cell indices are < 2^31 (make_layout)
+    uint32_t npos, nty4;     // remedy member-list traversal: positions (padded bricks), 4-row tiles in y
     FastDiv fnx, fny, fW;
     double dx, dy, delta, tol;
     int32_t slab;            // 1: z-slab of a sharded 3D grid, planes 0 and nz-1 are ghosts
@@ -109,6 +127,12 @@ struct KP {
     double *P0, *P1;         // P0 = caller phi, P1 = workspace copy
     const double *F;         // speed
     double *dd;              // delta / F (uniform solvers)
+    // speed palette (piecewise-constant F): 1-byte index per cell + exact coefficient table
+    uint8_t *pidx;
+    double *ptab;            // [PAL_MAX] delta/F_k (uniform) or F_k (anisotropic)
+    unsigned long long *phash;  // [PAL_SLOTS] F bit patterns (open addressing)
+    uint32_t *pslot;         // [PAL_SLOTS] slot -> palette index
+    uint32_t *pstate;        // [0] distinct count, [1] overflow, [2] palette in use
     const uint8_t *state;
     uint32_t *Bt;                 // touched bitmap (update step labels: not FAR)
     uint32_t *L0, *L1;            // update-step cell worklists
@@ -120,6 +144,11 @@ struct KP {
     uint32_t *R0b;       // R_0 (build / load)
     uint32_t *D0b, *D1b;  // D_r (decreased cells), double-buffered by round parity
     uint32_t *Fb;        // fixed = blocked | source | outside the row
+    // multi-rank (peer slabs): this rank owns planes [zg0, zg0 + nz) of the global grid
+    int32_t mr, q, R, pad2;
+    uint32_t gb0, gnb;     // this rank's CTAs: blockIdx.x in [gb0, gb0 + gnb)
+    Peer lo, hi;
+    Ctl *rank_ctl[EIK_MAX_RANKS];
 };
 
 
@@ -247,33 +276,57 @@ __device__ __forceinline__ unsigned long long globaltimer()
 
 constexpr unsigned EIK_EHANG = 5;  // device-side watchdog tripped (reported as a CUDA error)
 
-// Software grid barrier; all CTAs are co-resident (cooperative launch).
-// Returns false if the watchdog fired (a CTA did not arrive within ~10 s);
-// every caller then leaves the kernel so a logic error cannot wedge the GPU.
-__device__ __forceinline__ bool grid_barrier(Ctl *ctl)
+// Software barrier over this rank's CTAs (co-resident: cooperative launch) and,
+// in multi-rank mode, across ranks: the last CTA of a rank arrives at the world
+// counter (rank 0's control block), the last rank releases every rank's
+// generation word, each rank then releases its CTAs.  System-scope fences make
+// the data written before the barrier visible to peer GPUs.  Returns false if
+// the watchdog fired (nobody arrived within ~10 s); callers then leave the
+// kernel so a logic error cannot wedge the GPU.
+__device__ __forceinline__ bool spin_until_change(volatile unsigned *w, unsigned old, Ctl *ctl)
+{
+    const unsigned long long t0 = globaltimer();
+    while (*w == old) {
+        __nanosleep(32);
+        if (*(volatile unsigned *)&ctl->err == EIK_EHANG || globaltimer() - t0 > 10000000000ull) {
+            atomicExch(&ctl->err, EIK_EHANG);
+            return false;
+        }
+    }
+    return true;
+}
+
+__device__ __forceinline__ bool grid_barrier_n(Ctl *ctl, unsigned nblocks, const KP *p)
 {
     __shared__ unsigned s_ok;
     __syncthreads();
     if (threadIdx.x == 0) {
         volatile unsigned *vgen = &ctl->bar_gen;
         const unsigned gen = *vgen;
-        __threadfence();
+        if (p && p->mr) __threadfence_system();
+        else __threadfence();
         const unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
         unsigned ok = 1;
-        if (arrived == gridDim.x - 1) {
+        if (arrived == nblocks - 1) {
             atomicExch(&ctl->bar_count, 0u);
+            if (p && p->mr && p->R > 1) {
+                volatile unsigned *wg = &ctl->wgen;
+                const unsigned wgen = *wg;
+                __threadfence_system();
+                Ctl *c0 = p->rank_ctl[0];
+                if (atomicAdd(&c0->wcount, 1u) == (unsigned)p->R - 1) {
+                    atomicExch(&c0->wcount, 0u);
+                    __threadfence_system();
+                    for (int r = 0; r < p->R; ++r) atomicAdd(&p->rank_ctl[r]->wgen, 1u);
+                } else {
+                    ok = spin_until_change(wg, wgen, ctl);
+                }
+                __threadfence_system();
+            }
             __threadfence();
             atomicAdd(&ctl->bar_gen, 1u);
         } else {
-            const unsigned long long t0 = globaltimer();
-            while (*vgen == gen) {
-                __nanosleep(32);
-                if (*(volatile unsigned *)&ctl->err == EIK_EHANG || globaltimer() - t0 > 10000000000ull) {
-                    atomicExch(&ctl->err, EIK_EHANG);
-                    ok = 0;
-                    break;
-                }
-            }
+            ok = spin_until_change(vgen, gen, ctl);
         }
         __threadfence();
         s_ok = ok && *(volatile unsigned *)&ctl->err != EIK_EHANG;
@@ -281,6 +334,8 @@ __device__ __forceinline__ bool grid_barrier(Ctl *ctl)
     __syncthreads();
     return s_ok != 0;
 }
+
+__device__ __forceinline__ bool grid_barrier(Ctl *ctl) { return grid_barrier_n(ctl, gridDim.x, nullptr); }
 
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v)
@@ -303,6 +358,44 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, un
         for (int i = 0; i < WPB; ++i) t += sm[i];
     __syncthreads();
     return t;
+}
+
+constexpr int PAL_MAX = 255;     // palette entries (uint8 index)
+constexpr int PAL_SLOTS = 1024;  // hash slots
+constexpr unsigned long long PAL_EMPTY = ~0ull;
+
+// Per-cell coefficient of the local solver: d = delta/F (uniform) or F
+// (anisotropic), from the palette when the speed field has <= 255 distinct
+// values (same IEEE value, 1 byte of traffic instead of 8), else from the array.
+template <int SOL>
+__device__ __forceinline__ double coef(const KP &p, bool pal, uint32_t c)
+{
+    if (pal) return __ldg(p.ptab + __ldg(p.pidx + c));
+    return (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
+}
+
+__device__ __forceinline__ bool palette_on(const KP &p) { return p.pstate && __ldg(p.pstate + 2) != 0; }
+
+// Traversal order of the remedy member list: x-word columns of 4x4 (y, z) row
+// tiles (3D) or 16-row tiles (2D), so a CTA's consecutive members cover their
+// own y +- 1 / z +- 1 neighbour rows (L1 reuse).  Positions beyond the grid
+// (tile padding) map to an out-of-range word.
+template <int DIM>
+__device__ __forceinline__ uint32_t word_at(const KP &p, uint32_t l)
+{
+    const uint32_t in = l & 15u, t = l >> 4;
+    const uint32_t tile = t / p.W, wx = t - tile * p.W;
+    uint32_t y, z;
+    if (DIM == 3) {
+        const uint32_t tz = tile / p.nty4, ty = tile - tz * p.nty4;
+        y = ty * 4 + (in & 3u);
+        z = tz * 4 + (in >> 2);
+    } else {
+        y = tile * 16 + in;
+        z = 0;
+    }
+    if (y >= (uint32_t)p.ny || z >= (uint32_t)p.nz) return 0xffffffffu;
+    return (z * (uint32_t)p.ny + y) * p.W + wx;
 }
 
 struct WPos {
@@ -360,9 +453,13 @@ __device__ __forceinline__ void gather_issue(const KP &p, const double *__restri
         if (q.y + 1 < p.ny) s.n = ldcg(Pc + (c + p.nx32));
         if (DIM == 3) {
             if (q.z > 0) s.d = ldcg(Pc + (c - p.plane32));
+            else if (p.mr && p.lo.valid)  // multi-rank: neighbour's top plane, same buffer parity
+                s.d = ldcg((Pc == p.P0 ? p.lo.P0 : p.lo.P1) + (((p.lo.nz - 1) * (uint32_t)p.ny + q.y) * p.nx32 + q.x0 + lane));
             if (q.z + 1 < p.nz) s.u = ldcg(Pc + (c + p.plane32));
+            else if (p.mr && p.hi.valid)
+                s.u = ldcg((Pc == p.P0 ? p.hi.P0 : p.hi.P1) + (q.y * p.nx32 + q.x0 + lane));
         }
-        s.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
+        s.k = coef<SOL>(p, palette_on(p), c);
     }
 }
 
@@ -448,6 +545,72 @@ __global__ void k_seed(double *phi, uint8_t *state, const int64_t *idx, const do
     }
 }
 
+// ---- speed palette ---------------------------------------------------------
+__device__ __forceinline__ uint32_t pal_hash(unsigned long long k)
+{
+    k ^= k >> 33;
+    k *= 0xff51afd7ed558ccdull;
+    k ^= k >> 33;
+    return (uint32_t)k & (PAL_SLOTS - 1);
+}
+
+// Insert the distinct F bit patterns into an open-addressing table (warp-deduplicated).
+__global__ void k_palette_insert(KP p, int64_t n)
+{
+    const unsigned lane = lane_id();
+    for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
+        if (*(volatile uint32_t *)(p.pstate + 1)) return;  // overflow: give up
+        const int64_t i = i0 + lane;
+        const bool in = i < n;
+        const unsigned long long key = in ? (unsigned long long)__double_as_longlong(p.F[i]) : PAL_EMPTY;
+        const unsigned grp = __match_any_sync(FULL, key);
+        if (!in || lane != (unsigned)(__ffs(grp) - 1)) continue;
+        uint32_t h = pal_hash(key);
+        for (int probe = 0;; ++probe) {
+            if (probe == PAL_SLOTS) {
+                atomicExch(p.pstate + 1, 1u);
+                break;
+            }
+            const unsigned long long old = atomicCAS(p.phash + h, PAL_EMPTY, key);
+            if (old == PAL_EMPTY) {
+                if (atomicAdd(p.pstate, 1u) >= (unsigned)PAL_MAX) atomicExch(p.pstate + 1, 1u);
+                break;
+            }
+            if (old == key) break;
+            h = (h + 1) & (PAL_SLOTS - 1);
+        }
+    }
+}
+
+// Compact the occupied slots into palette indices; table = the solver coefficient
+// computed with the same IEEE operation as the per-cell array (delta / F).
+template <bool UNIFORM>
+__global__ void k_palette_finalize(KP p)
+{
+    __shared__ uint32_t cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const bool ok = p.pstate[1] == 0;
+    for (uint32_t s = threadIdx.x; s < (uint32_t)PAL_SLOTS; s += blockDim.x) {
+        const unsigned long long key = p.phash[s];
+        if (!ok || key == PAL_EMPTY) continue;
+        const uint32_t k = atomicAdd(&cnt, 1u);
+        p.pslot[s] = k;
+        const double f = __longlong_as_double((long long)key);
+        p.ptab[k] = UNIFORM ? p.delta / f : f;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) p.pstate[2] = ok ? 1u : 0u;
+}
+
+__device__ __forceinline__ uint8_t pal_index(const KP &p, double f)
+{
+    const unsigned long long key = (unsigned long long)__double_as_longlong(f);
+    uint32_t h = pal_hash(key);
+    while (__ldg(p.phash + h) != key) h = (h + 1) & (PAL_SLOTS - 1);
+    return (uint8_t)__ldg(p.pslot + h);
+}
+
 // One pass over all words: copy phi into the second buffer, d = delta / F,
 // touched = blocked, fixed = blocked | source, optionally clear set bitmaps.
 template <int DIM, bool UNIFORM>
@@ -456,6 +619,7 @@ __global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_
     const unsigned lane = lane_id();
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
+    const bool pal = palette_on(p);
     for (uint32_t w = gw; w < p.nwords; w += GW) {
         const WPos q = wpos<DIM>(p, w);
         const bool in = (q.rowm >> lane) & 1u;
@@ -464,7 +628,8 @@ __global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_
         if (in) {
             st = p.state[c];
             if (copy_phi) p.P1[c] = p.P0[c];
-            if (UNIFORM) p.dd[c] = p.delta / p.F[c];
+            if (pal) p.pidx[c] = pal_index(p, p.F[c]);
+            else if (UNIFORM) p.dd[c] = p.delta / p.F[c];
         }
         const uint32_t blk = __ballot_sync(FULL, in && st == ST_BLOCKED);
         const uint32_t src = __ballot_sync(FULL, in && st == ST_SOURCE);
@@ -472,6 +637,42 @@ __global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_
             const bool gh = ghost_plane(p, q.z);
             p.Fb[w] = gh ? FULL : (blk | src | ~q.rowm);  // lanes outside the row count as fixed
             if (build_touched) p.Bt[w] = gh ? 0u : blk;   // ghost bits record activation requests
+        }
+    }
+}
+
+// Multi-rank: write the seeds this rank owns (global linear index -> local).
+__global__ void k_seed_mr(double *phi, uint8_t *state, const int64_t *idx, const double *val, int64_t n, int64_t zg0,
+                          int64_t nzl, int64_t plane)
+{
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t z = idx[s] / plane;
+        if (z < zg0 || z >= zg0 + nzl) continue;
+        const int64_t c = idx[s] - zg0 * plane;
+        phi[c] = val[s];
+        state[c] = ST_SOURCE;
+    }
+}
+
+// Multi-rank initial activation: every seed (global index) activates the free
+// FAR neighbours this rank owns (E/ifim.py:97-102).
+__global__ void k_init_active_mr(KP p, const int64_t *seeds, int64_t nseeds, int64_t zg0, int64_t nz_global)
+{
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseeds; s += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = seeds[s];
+        const int64_t i = g % p.nx, r = g / p.nx, j = r % p.ny, k = r / p.ny;
+        const int64_t nb[6][3] = {{i - 1, j, k}, {i + 1, j, k}, {i, j - 1, k}, {i, j + 1, k}, {i, j, k - 1}, {i, j, k + 1}};
+        for (int t = 0; t < 6; ++t) {
+            const int64_t x = nb[t][0], y = nb[t][1], z = nb[t][2];
+            if (x < 0 || x >= p.nx || y < 0 || y >= p.ny || z < 0 || z >= nz_global) continue;
+            if (z < zg0 || z >= zg0 + p.nz) continue;  // owned by another rank
+            const int64_t e = ((z - zg0) * p.ny + y) * p.nx + x;
+            const uint8_t st = p.state[e];
+            if (st == ST_BLOCKED || st == ST_SOURCE) continue;
+            const uint32_t w = (uint32_t)(((z - zg0) * p.ny + y) * p.W + (x >> 5));
+            const uint32_t bit = 1u << (x & 31);
+            if (atomicOr(p.Bt + w, bit) & bit) continue;  // label != FAR
+            p.L0[atomicAdd(&p.ctl->len[0], 1u)] = (uint32_t)e;
         }
     }
 }
@@ -525,23 +726,46 @@ __global__ void k_init_active(KP p, const int64_t *seeds, int64_t nseeds)
 #ifndef UPD_MU
 #define UPD_MU 1  // active cells per thread per pass (2 measured slower: 47 vs 37 ms at 512^3)
 #endif
-template <int DIM, int SOL>
-__global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
+// Sum of a worklist-length slot over all ranks (multi-rank) or this rank.
+template <bool MR>
+__device__ __forceinline__ unsigned long long ranks_len(const KP &p, int slot)
+{
+    if (!MR) return vload(&p.ctl->len[slot]);
+    unsigned long long t = 0;
+    for (int r = 0; r < p.R; ++r) t += __ldcg(&p.rank_ctl[r]->len[slot]);
+    return t;
+}
+
+template <bool MR>
+__device__ __forceinline__ unsigned long long ranks_sum(const KP &p, const unsigned long long Ctl::*field, int slot)
+{
+    if (!MR) return vload(&(p.ctl->*field)) ;
+    unsigned long long t = 0;
+    for (int r = 0; r < p.R; ++r) t += vload(&(p.rank_ctl[r]->*field));
+    return t;
+}
+
+template <int DIM, int SOL, bool MR>
+__device__ __forceinline__ void update_body(const KP &p)
 {
     __shared__ unsigned sscan[WPB + 1];
     __shared__ unsigned long long sred[WPB];
     Ctl *ctl = p.ctl;
+    const unsigned gb = blockIdx.x - p.gb0, gnb = p.gnb ? p.gnb : gridDim.x;
+    const bool lead = gb == 0 && threadIdx.x == 0 && (!MR || p.q == 0);  // writes the global stats
     unsigned long long a_writes = 0, a_conv = 0;
+    if (MR && !grid_barrier_n(ctl, gnb, &p)) return;  // every rank's initial list is complete
     if (!p.slab) {
-        const unsigned n0 = vload(&ctl->len[0]);
+        const unsigned long long n0 = ranks_len<MR>(p, (int)(p.it0 % 3));
         if (n0 == 0) return;  // no initial active cell: zero iterations
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (lead) {
             if (p.hist_cap > 0) p.hist[0] = (int64_t)n0;
             ctl->sum = n0;
             ctl->peak = n0;
         }
     }
     const uint32_t nx = (uint32_t)p.nx, ny = (uint32_t)p.ny, nz = (uint32_t)p.nz;
+    const bool pal = palette_on(p);
     for (int64_t it = p.it0; it < p.it0 + p.max_it; ++it) {
         const int par = (int)(it & 1);
         const double *__restrict__ Pc = par ? p.P1 : p.P0;
@@ -550,7 +774,7 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
         uint32_t *Ln = par ? p.L0 : p.L1;
         unsigned *lenN = &ctl->len[(it + 1) % 3];
         const unsigned n = vload(&ctl->len[it % 3]);
-        for (unsigned base = blockIdx.x * (BLOCK * UPD_MU); base < n; base += gridDim.x * (BLOCK * UPD_MU)) {
+        for (unsigned base = gb * (BLOCK * UPD_MU); base < n; base += gnb * (BLOCK * UPD_MU)) {
             uint32_t c[UPD_MU], x[UPD_MU], y[UPD_MU], z[UPD_MU], r[UPD_MU];
             unsigned emit[UPD_MU];  // bit 0: stay; bits 1..6: activate W, E, S, N, D, U
             bool carry[UPD_MU], live[UPD_MU];
@@ -585,9 +809,13 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
                     if (y[u] + 1 < ny) t.n = __ldca(Pc + (cc + nx));
                     if (DIM == 3) {
                         if (z[u] > 0) t.d = __ldca(Pc + (cc - p.plane32));
+                        else if (MR && p.lo.valid)  // neighbour rank's top plane (peer memory)
+                            t.d = __ldcg((par ? p.lo.P1 : p.lo.P0) + (((p.lo.nz - 1) * ny + y[u]) * nx + x[u]));
                         if (z[u] + 1 < nz) t.u = __ldca(Pc + (cc + p.plane32));
+                        else if (MR && p.hi.valid)  // neighbour rank's bottom plane
+                            t.u = __ldcg((par ? p.hi.P1 : p.hi.P0) + (y[u] * nx + x[u]));
                     }
-                    t.k = (SOL == SOL_A2) ? __ldg(p.F + cc) : __ldg(p.dd + cc);
+                    t.k = coef<SOL>(p, pal, cc);
                 }
             }
 #pragma unroll
@@ -612,6 +840,20 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
                         old[k] = 0xffffffffu;
                         const bool inb = k == 0 ? x[u] > 0 : k == 1 ? x[u] + 1 < nx : k == 2 ? y[u] > 0
                                          : k == 3 ? y[u] + 1 < ny : k == 4 ? z[u] > 0 : z[u] + 1 < nz;
+                        if (MR && DIM == 3 && k >= 4 && !inb && nv[k] == INFINITY) {
+                            // the neighbour lies on an adjacent rank: activate it there (E/ifim.py:123-126)
+                            const Peer &pr = k == 4 ? p.lo : p.hi;
+                            if (pr.valid) {
+                                const uint32_t ze = k == 4 ? pr.nz - 1 : 0u;
+                                const uint32_t bit = 1u << (x[u] & 31);
+                                const uint32_t old2 = atomicOr(pr.Bt + (ze * ny + y[u]) * p.W + (x[u] >> 5), bit);
+                                if (!(old2 & bit)) {
+                                    uint32_t *Lp = par ? pr.L0 : pr.L1;
+                                    Lp[atomicAdd(&pr.ctl->len[(it + 1) % 3], 1u)] = (ze * ny + y[u]) * nx + x[u];
+                                }
+                            }
+                            continue;
+                        }
                         if (inb && nv[k] == INFINITY) {
                             const uint32_t xe = k == 0 ? x[u] - 1 : k == 1 ? x[u] + 1 : x[u];
                             const uint32_t re = k == 2 ? r[u] - 1 : k == 3 ? r[u] + 1 : k == 4 ? r[u] - ny
@@ -642,13 +884,13 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
                 }
             }
         }
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (gb == 0 && threadIdx.x == 0) {
             ctl->len[(it + 2) % 3] = 0;
         }
-        if (!grid_barrier(ctl)) return;
-        const unsigned m = vload(&ctl->len[(it + 1) % 3]);
+        if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
+        const unsigned long long m = ranks_len<MR>(p, (int)((it + 1) % 3));
         if (p.slab) continue;  // the host reduces the counts and decides
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (lead) {
             ctl->iters = it + 1;
             if (m) {
                 if (it + 1 < p.hist_cap) p.hist[it + 1] = (int64_t)m;
@@ -658,7 +900,7 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
         }
         if (m == 0) break;
         if (it + 1 >= p.cap) {  // E/ifim.py:106-110
-            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
+            if (gb == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
             break;
         }
     }
@@ -668,6 +910,20 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
         atomicAdd(&ctl->writes, tw);
         atomicAdd(&ctl->conv, tc);
     }
+}
+
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
+{
+    update_body<DIM, SOL, false>(p);
+}
+
+// Multi-rank: rank groups of one launch (emulation on one GPU, kps[] in device
+// memory) or one rank per GPU (kps[0]); peers through device-visible pointers.
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK, 3) k_update_mr(const KP *__restrict__ kps, uint32_t per_group)
+{
+    update_body<DIM, SOL, true>(kps[blockIdx.x / per_group]);
 }
 
 // ---------------------------------------------------------------------------
@@ -765,19 +1021,22 @@ constexpr int REM_PER = 4;  // bitmap words per thread in phase B
 #endif
 
 
-template <int DIM>
+template <int DIM, bool MR>
 __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint32_t *__restrict__ Dp,
-                                            uint32_t *Dc, uint32_t *ML, unsigned *lenR, unsigned *sscan)
+                                            uint32_t *Dc, uint32_t *ML, unsigned *lenR, unsigned *sscan, unsigned gb,
+                                            unsigned gnb)
 {
     const unsigned lane = lane_id();
     const uint32_t chunk = BLOCK * REM_PER;
     const uint32_t planeW = (uint32_t)p.ny * p.W;
-    for (uint32_t base = blockIdx.x * chunk; base < p.nwords; base += gridDim.x * chunk) {
-        uint32_t R[REM_PER], C[REM_PER];
+    const int ppar = (int)((r + 1) & 1);  // parity of D_{r-1}
+    for (uint32_t base = gb * chunk; base < p.npos; base += gnb * chunk) {
+        uint32_t R[REM_PER], C[REM_PER], WW[REM_PER];
         unsigned cnt = 0;
 #pragma unroll
         for (int k = 0; k < REM_PER; ++k) {
-            const uint32_t w = base + threadIdx.x * REM_PER + k;  // consecutive words: list stays word-sorted
+            const uint32_t w = word_at<DIM>(p, base + threadIdx.x * REM_PER + k);  // brick order (see word_at)
+            WW[k] = w;
             R[k] = C[k] = 0;
             if (w < p.nwords) {
                 if (r == 0) {
@@ -800,8 +1059,12 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
                     const uint32_t dn = y + 1 < p.ny ? __ldcg(Dp + w + p.W) : 0u;
                     uint32_t dd = 0, du = 0;
                     if (DIM == 3) {
-                        dd = z > 0 ? __ldcg(Dp + w - planeW) : 0u;
-                        du = z + 1 < p.nz ? __ldcg(Dp + w + planeW) : 0u;
+                        if (z > 0) dd = __ldcg(Dp + w - planeW);
+                        else if (MR && p.lo.valid)  // neighbour rank's top-plane decreases (peer memory)
+                            dd = __ldcg((ppar ? p.lo.D1b : p.lo.D0b) + ((p.lo.nz - 1) * (uint32_t)p.ny + y) * p.W + wx);
+                        if (z + 1 < p.nz) du = __ldcg(Dp + w + planeW);
+                        else if (MR && p.hi.valid)
+                            du = __ldcg((ppar ? p.hi.D1b : p.hi.D0b) + y * p.W + wx);
                     }
                     const uint32_t dil = (c << 1) | (c >> 1) | (dw >> 31) | (de << 31) | ds | dn | dd | du;
                     const bool gh = DIM == 3 && ghost_plane(p, z);
@@ -823,7 +1086,7 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
 #pragma unroll
         for (int k = 0; k < REM_PER; ++k) {
             unsigned todo = __ballot_sync(FULL, R[k] != 0);
-            const uint32_t w = base + threadIdx.x * REM_PER + k;
+            const uint32_t w = WW[k];
             const uint32_t row = fdiv(w, p.fW);
             const uint32_t c0 = row * p.nx32 + (w - row * p.W) * 32u;
             while (todo) {
@@ -844,25 +1107,33 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
 #ifndef REM_MINB
 #define REM_MINB 4
 #endif
-template <int DIM, int SOL>
-__global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy(KP p, const unsigned *skip)
+template <int DIM, int SOL, bool MR>
+__device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
 {
     __shared__ unsigned sscan[WPB + 1];
     __shared__ unsigned long long sred[WPB];
     if (skip && *skip) return;
     Ctl *ctl = p.ctl;
     const unsigned lane = lane_id();
+    const unsigned gb = blockIdx.x - p.gb0, gnb = p.gnb ? p.gnb : gridDim.x;
+    const bool lead = gb == 0 && threadIdx.x == 0 && (!MR || p.q == 0);
+    if (MR && !grid_barrier_n(ctl, gnb, &p)) return;  // every rank's build (R0) is complete
     if (!p.slab) {
-        const unsigned long long r0 = vload(&ctl->flagged);
+        unsigned long long r0 = 0;
+        if (MR) {
+            for (int q = 0; q < p.R; ++q) r0 += vload(&p.rank_ctl[q]->flagged);
+        } else {
+            r0 = vload(&ctl->flagged);
+        }
         if (r0 == 0) return;  // empty remedy set: zero rounds
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (lead) {
             ctl->peak = r0;
             ctl->sum = 0;
         }
     }
     const uint32_t nx = p.nx32, ny = (uint32_t)p.ny, nz = (uint32_t)p.nz;
-    const uint32_t gt = blockIdx.x * BLOCK + threadIdx.x, GT = gridDim.x * BLOCK;
     uint32_t *ML = p.L0;
+    const bool pal = palette_on(p);
     for (int64_t rr = p.it0; rr < p.it0 + p.max_it; ++rr) {
         const uint32_t r = (uint32_t)rr;
         const int par = (int)(r & 1);
@@ -872,30 +1143,38 @@ __global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy(KP p, const unsigned
         const uint32_t *Dp = par ? p.D0b : p.D1b;
         unsigned *lenR = &ctl->len[r % 3];
         // ---- phase B: members of R_r ----
-        rem_members<DIM>(p, r, Dp, Dc, ML, lenR, sscan);
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        rem_members<DIM, MR>(p, r, Dp, Dc, ML, lenR, sscan, gb, gnb);
+        if (gb == 0 && threadIdx.x == 0) {
             // slot (r+1)%3 of len / dsum was last read two rounds ago
             ctl->len[(r + 1) % 3] = 0;
             ctl->dsum[(r + 1) % 3] = 0;
         }
-        if (!grid_barrier(ctl)) return;
-        const unsigned m = vload(lenR);  // |R_r|
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
+        const unsigned m = vload(lenR);  // this rank's |R_r| (list length)
+        const unsigned long long mg = ranks_len<MR>(p, (int)(r % 3));  // global |R_r|
+        if (lead) {
             ctl->iters = r + 1;
-            ctl->sum += m;
-            if (m > ctl->peak) ctl->peak = m;
+            ctl->sum += mg;
+            if (mg > ctl->peak) ctl->peak = mg;
         }
         // ---- phase A: one local solve per member, REM_MU members per lane in flight ----
         unsigned long long a_dec = 0;
-        const uint32_t wbase = (gt - lane) * REM_MU, wstride = GT * REM_MU;
-        for (uint32_t i0 = wbase; i0 < m; i0 += wstride) {
+#ifdef REM_GRIDSTRIDE
+        const uint32_t wbase = ((gb * BLOCK + threadIdx.x) - lane) * REM_MU, wstride = gnb * BLOCK * REM_MU, mend = m;
+#else
+        // one contiguous segment of the (brick-ordered) list per CTA: L1 reuse of neighbour rows
+        const uint32_t seg = ((m + gnb - 1) / gnb + 32 * REM_MU - 1) / (32 * REM_MU) * (32 * REM_MU);
+        const uint32_t sbeg = gb * seg, mend = min(m, sbeg + seg);
+        const uint32_t wbase = sbeg + (threadIdx.x >> 5) * 32 * REM_MU, wstride = WPB * 32 * REM_MU;
+#endif
+        for (uint32_t i0 = wbase; i0 < mend; i0 += wstride) {
             uint32_t ent[REM_MU], rw[REM_MU], x[REM_MU];
             bool live[REM_MU];
             Sten s[REM_MU];
 #pragma unroll
             for (int u = 0; u < REM_MU; ++u) {
                 const uint32_t i = i0 + u * 32 + lane;
-                live[u] = i < m;
+                live[u] = i < mend;
                 ent[u] = live[u] ? __ldcg(ML + i) : 0u;
             }
 #pragma unroll
@@ -921,9 +1200,13 @@ __global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy(KP p, const unsigned
                     if (y + 1 < ny) t.n = __ldca(Pc + (c + nx));
                     if (DIM == 3) {
                         if (z > 0) t.d = __ldca(Pc + (c - p.plane32));
+                        else if (MR && p.lo.valid)  // neighbour rank's top plane (peer memory)
+                            t.d = __ldcg((par ? p.lo.P1 : p.lo.P0) + (((p.lo.nz - 1) * ny + y) * nx + x[u]));
                         if (z + 1 < nz) t.u = __ldca(Pc + (c + p.plane32));
+                        else if (MR && p.hi.valid)
+                            t.u = __ldcg((par ? p.hi.P1 : p.hi.P0) + (y * nx + x[u]));
                     }
-                    t.k = (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
+                    t.k = coef<SOL>(p, pal, c);
                 }
             }
 #pragma unroll
@@ -954,16 +1237,32 @@ __global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy(KP p, const unsigned
         }
         const unsigned long long td = block_sum(lane == 0 ? a_dec : 0ull, sred);
         if (threadIdx.x == 0 && td) atomicAdd(&ctl->dsum[r % 3], td);
-        if (!grid_barrier(ctl)) return;
-        const unsigned long long decs = vload(&ctl->dsum[r % 3]);
+        if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
+        unsigned long long decs = vload(&ctl->dsum[r % 3]);
+        if (MR) {
+            decs = 0;
+            for (int q = 0; q < p.R; ++q) decs += __ldcg(&p.rank_ctl[q]->dsum[r % 3]);
+        }
         if (p.slab) continue;  // the host reduces the counts and decides
-        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->writes += decs;
+        if (lead) ctl->writes += decs;
         if (decs == 0) break;
         if (r + 1 >= (uint32_t)p.cap) {  // E/ifim.py:185-189
-            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
+            if (gb == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
             break;
         }
     }
+}
+
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy(KP p, const unsigned *skip)
+{
+    remedy_body<DIM, SOL, false>(p, skip);
+}
+
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy_mr(const KP *__restrict__ kps, uint32_t per_group)
+{
+    remedy_body<DIM, SOL, true>(kps[blockIdx.x / per_group], nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -1130,8 +1429,8 @@ struct Layout {
     int64_t N;
     uint32_t W, nwords;
     size_t off_phi2, off_dd, off_bt, off_l0, off_l1;
-    size_t off_r0, off_d0, off_d1, off_f;
-    size_t off_hist, off_ctl_u, off_ctl_r, total;
+    size_t off_r0, off_d0, off_d1, off_f, off_pidx, off_ptab, off_phash, off_pslot, off_pstate;
+    size_t off_hist, off_ctl_u, off_ctl_r, off_kps, total;
     int64_t cap_upd, cap_rem;
 };
 
@@ -1168,9 +1467,15 @@ int make_layout(const eik_geom *g, Layout &L)
     L.off_d0 = o; o += al(bm);
     L.off_d1 = o; o += al(bm);
     L.off_f = o; o += al(bm);
+    L.off_pidx = o; o += al((size_t)L.N);
+    L.off_ptab = o; o += al(PAL_MAX * 8 + 8);
+    L.off_phash = o; o += al(PAL_SLOTS * 8);
+    L.off_pslot = o; o += al(PAL_SLOTS * 4);
+    L.off_pstate = o; o += al(16);
     L.off_hist = o; o += al((size_t)(L.cap_upd + 2) * 8);
     L.off_ctl_u = o; o += al(sizeof(Ctl));
     L.off_ctl_r = o; o += al(sizeof(Ctl));
+    L.off_kps = o; o += al(2 * EIK_MAX_RANKS * sizeof(KP));
     L.total = o;
     return EIK_OK;
 }
@@ -1194,6 +1499,13 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const doub
     p.fnx = make_fastdiv((uint32_t)g->nx);
     p.fny = make_fastdiv((uint32_t)g->ny);
     p.fW = make_fastdiv(L.W);
+    if (g->ndim == 3) {
+        p.nty4 = (uint32_t)((g->ny + 3) / 4);
+        p.npos = p.nty4 * 4 * (uint32_t)((g->nz + 3) / 4) * 4 * L.W;
+    } else {
+        p.nty4 = 0;
+        p.npos = (uint32_t)((g->ny + 15) / 16) * 16 * L.W;
+    }
     p.dx = g->dx; p.dy = g->dy; p.delta = g->dx; p.tol = tol;
     p.slab = (g->flags & EIK_GEOM_SLAB) ? 1 : 0;
     p.it0 = 0;
@@ -1214,6 +1526,11 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const doub
     p.D0b = (uint32_t *)(b + L.off_d0);
     p.D1b = (uint32_t *)(b + L.off_d1);
     p.Fb = (uint32_t *)(b + L.off_f);
+    p.pidx = (uint8_t *)(b + L.off_pidx);
+    p.ptab = (double *)(b + L.off_ptab);
+    p.phash = (unsigned long long *)(b + L.off_phash);
+    p.pslot = (uint32_t *)(b + L.off_pslot);
+    p.pstate = (uint32_t *)(b + L.off_pstate);
     return p;
 }
 
@@ -1260,11 +1577,40 @@ int coop_launch(K kernel, KP &p, const unsigned *skip, bool with_skip, cudaStrea
     return EIK_OK;
 }
 
+// Cooperative launch of a multi-rank kernel: nlocal rank groups, each with the
+// same number of CTAs; each CTA finds its rank's KP in kps_dev[blockIdx.x / per_group].
+template <typename K>
+int coop_launch_groups(K kernel, const KP *kps_dev, int nlocal, cudaStream_t st, int &per_group_out)
+{
+    int per_sm = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, BLOCK, 0);
+    if (e != cudaSuccess) return fail(EIK_ECUDA, "occupancy: %s", cudaGetErrorString(e));
+    const int total = per_sm * num_sms();
+    uint32_t per_group = (uint32_t)(total / nlocal);
+    if (per_group < 1) return fail(EIK_EINVAL, "too many ranks on one device");
+    per_group_out = (int)per_group;
+    dim3 grid(per_group * nlocal), block(BLOCK);
+    void *args[] = {(void *)&kps_dev, &per_group};
+    e = cudaLaunchCooperativeKernel((const void *)kernel, grid, block, args, 0, st);
+    if (e != cudaSuccess) return fail(EIK_ECUDA, "cooperative launch: %s", cudaGetErrorString(e));
+    return EIK_OK;
+}
+
 template <int DIM, int SOL>
 struct Engine {
     // phi copy (optional), d = delta/F, touched (optional) and the fixed brick bitmap
     static int prep(KP &p, bool copy_phi, bool touched, cudaStream_t st)
     {
+        CK(cudaMemsetAsync(p.pstate, 0, 16, st));
+        if (getenv("EIK_PALETTE")) {  // opt-in: measured slower on the 512^3 checkerboard (latency-bound gathers)
+            CK(cudaMemsetAsync(p.phash, 0xff, PAL_SLOTS * sizeof(unsigned long long), st));
+            const int64_t N = p.nx * p.ny * p.nz;
+            k_palette_insert<<<(int)std::min<int64_t>((N + 255) / 256, (int64_t)num_sms() * 8), 256, 0, st>>>(p, N);
+            CK(cudaGetLastError());
+            if (SOL == SOL_A2) k_palette_finalize<false><<<1, 256, 0, st>>>(p);
+            else k_palette_finalize<true><<<1, 256, 0, st>>>(p);
+            CK(cudaGetLastError());
+        }
         const int grid = stream_grid(p.nwords);
         if (SOL == SOL_A2) k_prep<DIM, false><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched);
         else k_prep<DIM, true><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched);
@@ -1285,7 +1631,12 @@ struct Engine {
     // remedy-set slots: counters (R0 is rewritten word by word)
     static int reset_set(KP &p, cudaStream_t st)
     {
-        CK(cudaMemsetAsync(p.ctl, 0, sizeof(Ctl), st));
+        if (p.mr) {  // keep bar_* / wcount / wgen: peers may already be waiting at the world barrier
+            CK(cudaMemsetAsync(&p.ctl->len[0], 0, offsetof(Ctl, nz_sectors) + sizeof(unsigned long long) -
+                                                     offsetof(Ctl, len), st));
+        } else {
+            CK(cudaMemsetAsync(p.ctl, 0, sizeof(Ctl), st));
+        }
         return EIK_OK;
     }
     static int build(KP &p, const double *Pc, const unsigned *skip, cudaStream_t st)
@@ -1309,6 +1660,14 @@ struct Engine {
         k_remedy_export<DIM><<<stream_grid(p.nwords), BLOCK, 0, st>>>(p, member);
         CK(cudaGetLastError());
         return EIK_OK;
+    }
+    static int update_mr(const KP *kps_dev, int nlocal, cudaStream_t st, int &per_group_out)
+    {
+        return coop_launch_groups(k_update_mr<DIM, SOL>, kps_dev, nlocal, st, per_group_out);
+    }
+    static int remedy_mr(const KP *kps_dev, int nlocal, cudaStream_t st, int &per_group_out)
+    {
+        return coop_launch_groups(k_remedy_mr<DIM, SOL>, kps_dev, nlocal, st, per_group_out);
     }
     static int fixpoint(KP &p, cudaStream_t st)
     {
@@ -1742,6 +2101,201 @@ int eik_max_residual(const eik_geom *g, const double *phi, const double *speed, 
     double r;
     memcpy(&r, &bits, 8);
     *out = r;  // 0.0 when no free finite cell (E/harness.py:158-159)
+    return EIK_OK;
+}
+
+// ---- multi-rank (peer slabs) -----------------------------------------------
+
+static Peer make_peer(const eik_geom *g, const eik_rank &rk, int use_remedy)
+{
+    Peer pr;
+    memset(&pr, 0, sizeof(pr));
+    eik_geom gl = *g;
+    gl.nz = rk.nz;
+    gl.flags = 0;
+    Layout L;
+    if (make_layout(&gl, L)) return pr;
+    char *b = (char *)rk.workspace;
+    pr.P0 = rk.phi0;
+    pr.P1 = (double *)(b + L.off_phi2);
+    pr.Bt = (uint32_t *)(b + L.off_bt);
+    pr.L0 = (uint32_t *)(b + L.off_l0);
+    pr.L1 = (uint32_t *)(b + L.off_l1);
+    pr.D0b = (uint32_t *)(b + L.off_d0);
+    pr.D1b = (uint32_t *)(b + L.off_d1);
+    pr.ctl = (Ctl *)(b + (use_remedy ? L.off_ctl_r : L.off_ctl_u));
+    pr.nz = (uint32_t)rk.nz;
+    pr.valid = 1;
+    return pr;
+}
+
+struct MrCtx {
+    eik_geom gl;
+    Layout L;
+    KP kp;
+};
+
+static int mr_setup(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t q, const double *speed,
+                    uint8_t *state, double tol, int use_remedy, MrCtx &m)
+{
+    if (!g || g->ndim != 3 || g->flags) return fail(EIK_EINVAL, "multi-rank solves take the global 3D geometry");
+    if (R < 1 || R > EIK_MAX_RANKS) return fail(EIK_EINVAL, "1 <= ranks <= %d", EIK_MAX_RANKS);
+    int64_t nzsum = 0;
+    for (int r = 0; r < R; ++r) {
+        if (ranks[r].nz < 1 || !ranks[r].workspace || !ranks[r].phi0) return fail(EIK_EINVAL, "bad rank %d", r);
+        nzsum += ranks[r].nz;
+    }
+    if (nzsum != g->nz) return fail(EIK_EINVAL, "rank slabs cover %lld planes, grid has %lld", (long long)nzsum,
+                                    (long long)g->nz);
+    int64_t zg0 = 0;
+    for (int r = 0; r < q; ++r) zg0 += ranks[r].nz;
+    m.gl = *g;
+    m.gl.nz = ranks[q].nz;
+    int rc = make_layout(&m.gl, m.L);
+    if (rc) return rc;
+    char *b = (char *)ranks[q].workspace;
+    const int64_t s3 = g->nx + g->ny + g->nz;  // caps of the GLOBAL grid
+    m.kp = make_kp(&m.gl, m.L, ranks[q].workspace, ranks[q].phi0, speed, state, tol,
+                   (Ctl *)(b + (use_remedy ? m.L.off_ctl_r : m.L.off_ctl_u)), use_remedy ? 20 * s3 : 40 * s3);
+    m.kp.mr = 1;
+    m.kp.q = q;
+    m.kp.R = R;
+    if (q > 0) m.kp.lo = make_peer(g, ranks[q - 1], use_remedy);
+    if (q + 1 < R) m.kp.hi = make_peer(g, ranks[q + 1], use_remedy);
+    for (int r = 0; r < R; ++r) m.kp.rank_ctl[r] = make_peer(g, ranks[r], use_remedy).ctl;
+    (void)zg0;
+    return EIK_OK;
+}
+
+int eik_mr_prepare(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_begin, int32_t r_end,
+                   const double *const *speed, uint8_t *const *state, const int64_t *seeds, const double *seed_val,
+                   int64_t nseeds, double tol, void *stream)
+{
+    if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
+    if (r_begin < 0 || r_end > R || r_begin >= r_end) return fail(EIK_EINVAL, "bad local rank range");
+    if (nseeds < 1 || !seeds || !seed_val) return fail(EIK_EINVAL, "boundary condition has no seeds");
+    cudaStream_t st = (cudaStream_t)stream;
+    for (int q = r_begin; q < r_end; ++q) {
+        MrCtx m;
+        int rc = mr_setup(g, R, ranks, q, speed[q - r_begin], state[q - r_begin], tol, 0, m);
+        if (rc) return rc;
+        char *b = (char *)ranks[q].workspace;
+        CK(cudaMemsetAsync(b + m.L.off_ctl_u, 0, sizeof(Ctl), st));
+        CK(cudaMemsetAsync(b + m.L.off_ctl_r, 0, sizeof(Ctl), st));
+        int64_t zg0 = 0;
+        for (int r = 0; r < q; ++r) zg0 += ranks[r].nz;
+        k_seed_mr<<<(int)std::min<int64_t>((nseeds + 255) / 256, 1024), 256, 0, st>>>(
+            ranks[q].phi0, state[q - r_begin], seeds, seed_val, nseeds, zg0, ranks[q].nz, g->nx * g->ny);
+        CK(cudaGetLastError());
+        KP p = m.kp;
+        rc = dispatch(&m.gl, [&](auto E) { return E.prep(p, true, true, st); });
+        if (rc) return rc;
+        k_init_active_mr<<<(int)std::min<int64_t>((nseeds + 255) / 256, 1024), 256, 0, st>>>(p, seeds, nseeds, zg0,
+                                                                                            g->nz);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(st));
+    return EIK_OK;
+}
+
+int eik_mr_run(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_begin, int32_t r_end,
+               const double *const *speed, uint8_t *const *state, double tol, int64_t *history, int64_t history_cap,
+               eik_stats *out, void *stream)
+{
+    if (r_begin < 0 || r_end > R || r_begin >= r_end) return fail(EIK_EINVAL, "bad local rank range");
+    if (!out) return fail(EIK_EINVAL, "null stats");
+    cudaStream_t st = (cudaStream_t)stream;
+    memset(out, 0, sizeof(*out));
+    const int nl = r_end - r_begin;
+    Events ev;
+    ev.rec(0, st);
+    // update step: one cooperative launch over the local ranks
+    std::vector<MrCtx> mu(nl), mrm(nl);
+    for (int i = 0; i < nl; ++i) {
+        int rc = mr_setup(g, R, ranks, r_begin + i, speed[i], state[i], tol, 0, mu[i]);
+        if (rc) return rc;
+        rc = mr_setup(g, R, ranks, r_begin + i, speed[i], state[i], tol, 1, mrm[i]);
+        if (rc) return rc;
+        mu[i].kp.gb0 = mrm[i].kp.gb0 = 0;  // set after the group size is known
+    }
+    char *b0 = (char *)ranks[r_begin].workspace;
+    KP *kps_dev = (KP *)(b0 + mu[0].L.off_kps);
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_mr<3, SOL_U3>, BLOCK, 0));
+    uint32_t pg = (uint32_t)(per_sm * num_sms() / nl);
+    std::vector<KP> host(nl);
+    for (int i = 0; i < nl; ++i) {
+        host[i] = mu[i].kp;
+        host[i].gb0 = pg * i;
+        host[i].gnb = pg;
+    }
+    CK(cudaMemcpyAsync(kps_dev, host.data(), sizeof(KP) * nl, cudaMemcpyHostToDevice, st));
+    int pgo = 0;
+    int rc = Engine<3, SOL_U3>::update_mr(kps_dev, nl, st, pgo);
+    if (rc) return rc;
+    if ((uint32_t)pgo != pg) return fail(EIK_ECUDA, "group size mismatch");
+    ev.rec(1, st);
+    // build: per local rank (reads the neighbours' final phi; the update's last world barrier ordered it)
+    for (int i = 0; i < nl; ++i) {
+        KP p = mrm[i].kp;
+        rc = Engine<3, SOL_U3>::build(p, p.P0, nullptr, st);
+        if (rc) return rc;
+    }
+    ev.rec(2, st);
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_remedy_mr<3, SOL_U3>, BLOCK, 0));
+    pg = (uint32_t)(per_sm * num_sms() / nl);
+    for (int i = 0; i < nl; ++i) {
+        host[i] = mrm[i].kp;
+        host[i].gb0 = pg * i;
+        host[i].gnb = pg;
+    }
+    KP *kps_dev_r = kps_dev + EIK_MAX_RANKS;
+    CK(cudaMemcpyAsync(kps_dev_r, host.data(), sizeof(KP) * nl, cudaMemcpyHostToDevice, st));
+    rc = Engine<3, SOL_U3>::remedy_mr(kps_dev_r, nl, st, pgo);
+    if (rc) return rc;
+    ev.rec(3, st);
+    // global stats live in rank 0's control blocks; errors in any local rank's
+    Ctl cu0, cr0;
+    CK(cudaMemcpyAsync(&cu0, mu[0].kp.rank_ctl[0], sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&cr0, mrm[0].kp.rank_ctl[0], sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    unsigned long long writes = 0, conv = 0, freec = 0, flagged = 0;
+    for (int r = 0; r < R; ++r) {
+        Ctl cu, cr;
+        CK(cudaMemcpyAsync(&cu, mu[0].kp.rank_ctl[r], sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(&cr, mrm[0].kp.rank_ctl[r], sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if ((rc = check_hang(cu, "multi-rank update step")) || (rc = check_hang(cr, "multi-rank remedy step")))
+            return rc;
+        if (cu.err == EIK_ECAP) return fail(EIK_ECAP, "active list did not drain");
+        if (cr.err == EIK_ECAP) return fail(EIK_ECAP, "remedy set did not drain");
+        writes += cu.writes;
+        conv += cu.conv;
+        freec += cr.free_cells;
+        flagged += cr.flagged;
+    }
+    fill_update_stats(cu0, out);
+    out->converged = (int64_t)conv;
+    out->build_calls = (int64_t)freec;
+    out->remedy_size = (int64_t)flagged;
+    out->rem_iterations = (int64_t)cr0.iters;
+    out->rem_calls = (int64_t)cr0.sum;
+    out->peak_remedy = (int64_t)cr0.peak;
+    out->iterations = out->upd_iterations + out->rem_iterations;
+    out->solver_calls = out->upd_calls + out->build_calls + out->rem_calls;
+    out->phi_writes = (int64_t)(writes + cr0.writes);
+    out->upd_ms = ev.ms(0, 1);
+    out->build_ms = ev.ms(1, 2);
+    out->rem_ms = ev.ms(2, 3);
+    out->total_ms = ev.ms(0, 3);
+    out->gpu_launches = 2 + nl;
+    if (history && history_cap > 0 && cu0.iters > 0) {
+        eik_geom g0 = *g;
+        g0.nz = ranks[0].nz;
+        Layout L0;
+        if ((rc = make_layout(&g0, L0))) return rc;
+        const int64_t n = std::min<int64_t>((int64_t)cu0.iters, history_cap);
+        CK(cudaMemcpy(history, (char *)ranks[0].workspace + L0.off_hist, (size_t)n * 8, cudaMemcpyDeviceToHost));
+    }
     return EIK_OK;
 }
 

@@ -1,0 +1,64 @@
+"""Peer-memory slabs (the multi-GPU kernels) emulated on one GPU: R ranks as CTA
+groups of one cooperative launch, neighbour planes read through device
+pointers.  Bit-identical to the single-device solve and to the oracle."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2106_15869_b200 as eik
+from oracle import cpu
+from paper_2106_15869_b200.slab_peer import solve_emulated
+
+pytestmark = pytest.mark.gpu
+
+
+def problem(kind):
+    rng = np.random.default_rng(5)
+    if kind == "checker":
+        nz, ny, nx = 24, 20, 40
+        kk, jj, ii = np.mgrid[0:nz, 0:ny, 0:nx]
+        F = np.where(((ii // 4) + (jj // 4) + (kk // 4)) % 2 == 0, 1.0, 0.01)
+    elif kind == "walls":
+        nz, ny, nx = 13, 16, 37
+        kk, jj, ii = np.mgrid[0:nz, 0:ny, 0:nx]
+        F = np.exp(0.5 * np.sin(0.5 * ii) * np.cos(0.3 * jj + 0.2 * kk))
+        F[6, 3:14, 2:30] = 0.0
+        F[3, 0:10, 10:12] = 0.0
+    else:
+        nz, ny, nx = 20, 18, 33
+        F = np.ones((nz, ny, nx))
+    free = np.flatnonzero(F.ravel() > 0)
+    seeds = [(int(c), float(v)) for c, v in zip(rng.choice(free, 4, replace=False), (0.0, 0.3, 0.0, 1.0))]
+    state = np.where(F == 0, 4, 0).astype(np.uint8)
+    return (nz, ny, nx), 0.5, F, state, seeds
+
+
+@pytest.mark.parametrize("R", [1, 2, 3, 5])
+@pytest.mark.parametrize("kind", ["checker", "walls", "const"])
+def test_peer_slabs_bit_identical(R, kind):
+    shape, h, F, state, seeds = problem(kind)
+    ref = cpu.solve_ifim(shape, h, F, [c for c, _ in seeds], [v for _, v in seeds], state=state, threads=8)
+    dev = torch.device("cuda:0")
+    phi, st, state_out = solve_emulated(shape, h, torch.as_tensor(F, device=dev), torch.as_tensor(state, device=dev),
+                                        seeds, R)
+    assert np.array_equal(phi.cpu().numpy().view(np.uint64), ref.phi.view(np.uint64))
+    assert (st.iterations, st.solver_calls, st.peak_active, st.peak_remedy) == (
+        ref.stats["iterations"], ref.stats["solver_calls"], ref.stats["peak_active"], ref.stats["peak_remedy"])
+    assert st.active_history == ref.active_history
+    assert st.phi_writes == ref.stats["phi_writes"]
+    assert np.array_equal(state_out.cpu().numpy(), ref.state)
+
+
+@pytest.mark.slow
+def test_peer_slabs_512_matches_single():
+    n = 256
+    k = torch.arange(n, device="cuda") // (n // 16)
+    F = torch.where(((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2) == 0, 1.0, 0.01).double()
+    state = torch.zeros((n, n, n), dtype=torch.uint8, device="cuda")
+    c = n // 2
+    g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), np.inf, dtype=torch.float64, device="cuda"),
+                   F, state.clone())
+    single = eik.solve_ifim(g, eik.seed_point(g, (c, c, c), 0.0))
+    phi, st, _ = solve_emulated((n, n, n), 1.0, F, state, [((c * n + c) * n + c, 0.0)], 4)
+    assert torch.equal(phi, single.phi)
+    assert st.solver_calls == single.stats.solver_calls and st.active_history == single.stats.active_history
