@@ -14,10 +14,13 @@ SURVEY.md §8d).  `value` = total node updates / device time over all ranks.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--size 512] [--impl ours|reference]
 
-N > 1 (torchrun): ONE 512^3 grid is z-slab sharded over the ranks
-(paper_2106_15869_b200/slab.py: one ghost-plane / request / decrease-plane
-exchange per step over NCCL, counts all-reduced; strong scaling); the time is
-the max over ranks.  --slabs runs that protocol on one GPU.  --impl reference
+N > 1 (torchrun): ONE 512^3 grid is z-slab sharded over the ranks (strong
+scaling), by default in the fused peer-memory kernels
+(paper_2106_15869_b200/slab_peer.py: neighbour planes read over NVLink inside
+the persistent kernels, device-side cross-rank barrier); --host-slabs selects
+the host-driven protocol (paper_2106_15869_b200/slab.py: one ghost-plane /
+request / decrease-plane exchange per step over NCCL).  The time is the max
+over ranks.  --slabs runs that protocol on one GPU.  --impl reference
 times the CPU oracle port of the reference algorithm (oracle/eik_oracle.c,
 OpenMP on all host cores) on a bounded sample of the same workload family.
 """
@@ -231,6 +234,49 @@ def make_slab_step(torch, dev, n, c, F, world, rank):
     return step
 
 
+def peer_slabs_possible(torch, dev, world, local):
+    """Every rank can map every other rank's memory (NVLink / NVSwitch), agreed over all ranks."""
+    import torch.distributed as dist
+
+    ok = 1
+    try:
+        import torch.distributed._symmetric_memory  # noqa: F401
+
+        for o in range(torch.cuda.device_count()):
+            if o != local and o < world and not torch.cuda.can_device_access_peer(local, o):
+                ok = 0
+    except Exception:
+        ok = 0
+    t = torch.tensor([ok], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
+def make_peer_step(torch, dev, n, c, F, world, rank):
+    """This rank's share of ONE z-sharded solve in the fused peer-memory kernels
+    (paper_2106_15869_b200/slab_peer.py): neighbour planes read over NVLink inside the
+    persistent kernels, one device-side cross-rank barrier per iteration."""
+    from paper_2106_15869_b200.slab import SlabPartition
+    from paper_2106_15869_b200.slab_peer import DistributedSlabs
+
+    ds = DistributedSlabs((n, n, n), 1.0)
+    z0, z1 = SlabPartition(n, world).bounds(rank)
+    sp = F[z0:z1].contiguous()
+    st0 = torch.zeros((z1 - z0, n, n), dtype=torch.uint8, device=dev)
+    st = torch.empty_like(st0)
+    seeds = [((c * n + c) * n + c, 0.0)]
+
+    def step():
+        st.copy_(st0)
+        _, s = ds.solve(sp, st, seeds)
+        ph = s.phases
+        rem_writes = s.phi_writes - (ph["update"]["solver_calls"] - ph["update"]["converged"])
+        return StepStats(s.solver_calls, s.iterations, s.peak_remedy, ph["remedy"]["solver_calls"], rem_writes,
+                         s.device_ms["remedy"], s.gpu_launches, {k: round(v, 3) for k, v in s.device_ms.items()})
+
+    return step
+
+
 def run_ours(args):
     import torch
 
@@ -252,7 +298,13 @@ def run_ours(args):
     kk = torch.arange(n, device=dev) // blk
     F = torch.where(((kk[:, None, None] + kk[None, :, None] + kk[None, None, :]) % 2) == 0, 1.0, 0.01).double()
     slabs = world > 1 or args.slabs
-    step = make_slab_step(torch, dev, n, c, F, world, rank) if slabs else make_single_step(eik, torch, dev, n, c, F)
+    mode = "single"
+    if world > 1 and not args.host_slabs and peer_slabs_possible(torch, dev, world, local):
+        step, mode = make_peer_step(torch, dev, n, c, F, world, rank), "peer"
+    elif slabs:
+        step, mode = make_slab_step(torch, dev, n, c, F, world, rank), "host"
+    else:
+        step = make_single_step(eik, torch, dev, n, c, F)
 
     for _ in range(args.warmup):
         r = step()
@@ -288,10 +340,14 @@ def run_ours(args):
     clocks = clk.summary()
 
     # roofline of the dominant kernel (k_remedy, this rank): algorithmic bytes (SURVEY.md §8d:
-    # 8 B x (2 x solver_calls + phi_writes) of the remedy phase) / its CUDA-event duration
+    # 8 B x (2 x solver_calls + phi_writes) of the remedy phase) / its CUDA-event duration.
+    # Peer mode: the counts are global and the ranks run in lockstep, so the figure is the
+    # aggregate over the ranks against the aggregate peak.
     alg_bytes = 8.0 * (2 * r.rem_calls + r.rem_writes)
     rem_s = statistics.median(rem_ms) / 1e3
     peak, peak_src = hbm_peak()
+    if mode == "peer":
+        peak, peak_src = peak * world, peak_src + f" x {world} ranks"
     achieved = alg_bytes / rem_s / 1e9 if rem_s > 0 else None
     traffic = traffic_from_profiles(workload) if not slabs else None
 
@@ -308,7 +364,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload, "size": n, "solver_calls_per_step": calls,
                        "iterations": r.iterations, "peak_remedy": r.peak_remedy,
-                       "parallelism": f"z-slabs x{world} (host-driven exchange)" if slabs else "single",
+                       "parallelism": {"peer": f"z-slabs x{world} (peer-memory fused kernels)",
+                                       "host": f"z-slabs x{world} (host-driven exchange)"}.get(mode, "single"),
                        "l2": "inputs larger than L2 (phi 1 GiB fp64 per field at 512^3)",
                        "phase_ms": r.phase_ms},
             "wall_clock_to_convergence_ms": ms / args.steps,
@@ -369,6 +426,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--slabs", action="store_true", help="use the z-slab protocol even on one GPU")
+    ap.add_argument("--host-slabs", action="store_true", help="N>1: host-driven NCCL slabs instead of peer memory")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -314,10 +314,10 @@ __device__ __forceinline__ bool grid_barrier_n(Ctl *ctl, unsigned nblocks, const
                 const unsigned wgen = *wg;
                 __threadfence_system();
                 Ctl *c0 = p->rank_ctl[0];
-                if (atomicAdd(&c0->wcount, 1u) == (unsigned)p->R - 1) {
-                    atomicExch(&c0->wcount, 0u);
+                if (atomicAdd_system(&c0->wcount, 1u) == (unsigned)p->R - 1) {
+                    atomicExch_system(&c0->wcount, 0u);
                     __threadfence_system();
-                    for (int r = 0; r < p->R; ++r) atomicAdd(&p->rank_ctl[r]->wgen, 1u);
+                    for (int r = 0; r < p->R; ++r) atomicAdd_system(&p->rank_ctl[r]->wgen, 1u);
                 } else {
                     ok = spin_until_change(wg, wgen, ctl);
                 }
@@ -503,6 +503,7 @@ constexpr uint32_t CARRY = 0x80000000u;
 
 // Block-wide exclusive scan of a per-thread count plus one global reservation:
 // returns this thread's first slot in the global list whose length is *glen.
+template <bool SYS = false>
 __device__ __forceinline__ unsigned block_reserve(unsigned v, unsigned *glen, unsigned *sscan)
 {
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -521,7 +522,7 @@ __device__ __forceinline__ unsigned block_reserve(unsigned v, unsigned *glen, un
             sscan[i] = acc;
             acc += t;
         }
-        sscan[WPB] = acc ? atomicAdd(glen, acc) : 0u;
+        sscan[WPB] = acc ? (SYS ? atomicAdd_system(glen, acc) : atomicAdd(glen, acc)) : 0u;
     }
     __syncthreads();
     const unsigned pos = sscan[WPB] + sscan[warp] + inc - v;
@@ -846,10 +847,10 @@ __device__ __forceinline__ void update_body(const KP &p)
                             if (pr.valid) {
                                 const uint32_t ze = k == 4 ? pr.nz - 1 : 0u;
                                 const uint32_t bit = 1u << (x[u] & 31);
-                                const uint32_t old2 = atomicOr(pr.Bt + (ze * ny + y[u]) * p.W + (x[u] >> 5), bit);
+                                const uint32_t old2 = atomicOr_system(pr.Bt + (ze * ny + y[u]) * p.W + (x[u] >> 5), bit);
                                 if (!(old2 & bit)) {
                                     uint32_t *Lp = par ? pr.L0 : pr.L1;
-                                    Lp[atomicAdd(&pr.ctl->len[(it + 1) % 3], 1u)] = (ze * ny + y[u]) * nx + x[u];
+                                    Lp[atomicAdd_system(&pr.ctl->len[(it + 1) % 3], 1u)] = (ze * ny + y[u]) * nx + x[u];
                                 }
                             }
                             continue;
@@ -859,7 +860,9 @@ __device__ __forceinline__ void update_body(const KP &p)
                             const uint32_t re = k == 2 ? r[u] - 1 : k == 3 ? r[u] + 1 : k == 4 ? r[u] - ny
                                                 : k == 5 ? r[u] + ny : r[u];
                             const uint32_t bit = 1u << (xe & 31);
-                            old[k] = atomicOr(p.Bt + re * p.W + (xe >> 5), bit) | ~bit;
+                            // boundary planes are also activated by the neighbouring ranks: system scope
+                            old[k] = ((MR && (z[u] <= 1u || z[u] + 2u >= nz)) ? atomicOr_system(p.Bt + re * p.W + (xe >> 5), bit)
+                                                                               : atomicOr(p.Bt + re * p.W + (xe >> 5), bit)) | ~bit;
                             // slab mode: a ghost-plane target is an activation request for its owner
                             if (DIM == 3 && k >= 4 && ghost_plane(p, k == 4 ? z[u] - 1 : z[u] + 1)) old[k] = 0xffffffffu;
                         }
@@ -872,7 +875,7 @@ __device__ __forceinline__ void update_body(const KP &p)
             unsigned tot = 0;
 #pragma unroll
             for (int u = 0; u < UPD_MU; ++u) tot += __popc(emit[u]);
-            unsigned pos = block_reserve(tot, lenN, sscan);
+            unsigned pos = block_reserve<MR>(tot, lenN, sscan);  // peers append to lenN too
 #pragma unroll
             for (int u = 0; u < UPD_MU; ++u) {
                 if (emit[u] & 1u) Ln[pos++] = c[u] | CARRY;

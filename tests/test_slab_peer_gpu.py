@@ -62,3 +62,19 @@ def test_peer_slabs_512_matches_single():
     phi, st, _ = solve_emulated((n, n, n), 1.0, F, state, [((c * n + c) * n + c, 0.0)], 4)
     assert torch.equal(phi, single.phi)
     assert st.solver_calls == single.stats.solver_calls and st.active_history == single.stats.active_history
+
+
+def test_distributed_peer_slabs_symmetric_memory():
+    """DistributedSlabs through torch symmetric memory under torchrun (1 rank per GPU present)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    n = torch.cuda.device_count()
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+                        "--master-addr", "127.0.0.1", "--master-port", "29533",
+                        os.path.join(root, "tools", "peer_slab_check.py")],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert "bit-identical=True" in r.stdout
