@@ -75,6 +75,9 @@ struct Ctl {
     unsigned long long nz_sectors;
     unsigned wcount;                // multi-rank: world-barrier arrivals (rank 0's copy is used)
     unsigned wgen;                  // multi-rank: this rank's world-barrier generation
+#ifdef EIK_DIAG
+    unsigned long long dg[4][26];   // remedy rounds by log2|R_r|: count, phase B ns, phase A ns, members
+#endif
 };
 
 constexpr int EIK_MAX_RANKS = 16;
@@ -116,10 +119,10 @@ __device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv &f)
 
 struct KP {
     int64_t nx, ny, nz, plane;
-    uint32_t W, nwords, nrows, pad0;
+    uint32_t W, nwords, nrows, ncells;  // ncells < 2^31
     uint32_t nx32, plane32;  // cell indices are < 2^31 (make_layout)
     uint32_t npos, nty4;     // remedy member-list traversal: positions (padded bricks), 4-row tiles in y
-    FastDiv fnx, fny, fW;
+    FastDiv fnx, fny, fW, fnty4;
     double dx, dy, delta, tol;
     int32_t slab;            // 1: z-slab of a sharded 3D grid, planes 0 and nz-1 are ghosts
     int32_t pad1;
@@ -172,6 +175,21 @@ __device__ __forceinline__ double sqrt_rn(double x)
     return r;
 }
 __device__ __forceinline__ double sqrt_pos(double x) { return x > 0.0 ? sqrt_rn(x > 0.0 ? x : 1.0) : 0.0; }
+
+// x / 3.0 correctly rounded without the division sequence (Markstein): inv3 =
+// RN(1/3) has relative error 2^-54, so q = RN(x * inv3) is within 3/4 ulp of
+// x/3 (faithful), r = x - 3q is exact under FMA, and RN(q + r * inv3) is the
+// correctly rounded quotient; x/3 is never a rounding tie.  Tiny (subnormal
+// quotient), zero and non-finite dividends take the IEEE division.  Checked
+// bit-exact against x / 3.0 on 3.4e10 values (tools/cuda/check_div3.cu).
+__device__ __forceinline__ double div3_rn(double x)
+{
+    if (!(x >= 0x1p-900) || !(x < INFINITY)) return x / 3.0;
+    const double inv3 = 0x1.5555555555555p-2;
+    const double q = __dmul_rn(x, inv3);
+    const double r = __fma_rn(-q, 3.0, x);
+    return __fma_rn(r, inv3, q);
+}
 
 // E/_kernels.py:47-58 (_update_uniform_batch), d = delta / f
 __device__ __forceinline__ double upd2u(double a, double b, double d)
@@ -240,7 +258,7 @@ __device__ __forceinline__ double upd3u(double px, double py, double pz, double 
     // r3 is only ever selected with a3 finite; an infinite dividend would take
     // the division slow path for a value nobody reads
     const double x3 = s3 + sqrt_pos(disc3);
-    const double r3 = a1 + (x3 < INFINITY ? x3 : 0.0) / 3.0;
+    const double r3 = a1 + div3_rn(x3 < INFINITY ? x3 : 0.0);
     const bool quick = (a1 == INFINITY) || (k0 == 3 && !F3 && r3 >= a3);
     if (__all_sync(__activemask(), quick)) return a1 == INFINITY ? INFINITY : r3;
     // branch 2 (E/local_solver.py:136-151) and branch 1 (:152-157)
@@ -384,10 +402,10 @@ template <int DIM>
 __device__ __forceinline__ uint32_t word_at(const KP &p, uint32_t l)
 {
     const uint32_t in = l & 15u, t = l >> 4;
-    const uint32_t tile = t / p.W, wx = t - tile * p.W;
+    const uint32_t tile = fdiv(t, p.fW), wx = t - tile * p.W;
     uint32_t y, z;
     if (DIM == 3) {
-        const uint32_t tz = tile / p.nty4, ty = tile - tz * p.nty4;
+        const uint32_t tz = fdiv(tile, p.fnty4), ty = tile - tz * p.nty4;
         y = ty * 4 + (in & 3u);
         z = tz * 4 + (in >> 2);
     } else {
@@ -1022,6 +1040,9 @@ constexpr int REM_PER = 4;  // bitmap words per thread in phase B
 #ifndef REM_MU
 #define REM_MU 2            // phase A: members per lane in flight
 #endif
+#ifndef REM_PREF
+#define REM_PREF 0          // phase A: 1 = list entries one iteration ahead, 2 = + L2 prefetch of their rows
+#endif
 
 
 template <int DIM, bool MR>
@@ -1076,7 +1097,7 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
                 }
                 Dc[w] = 0;  // D_r is accumulated by phase A with atomicOr
                 cnt += __popc(R[k]);
-#ifdef EIK_DIAG
+#ifdef EIK_DIAG_SECT
                 if (R[k]) {
                     atomicAdd(&p.ctl->nz_words, 1ull);
                     atomicAdd(&p.ctl->nz_sectors, (unsigned long long)__popc((R[k] | (R[k] >> 1) | (R[k] >> 2) | (R[k] >> 3)) & 0x11111111u));
@@ -1139,6 +1160,11 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
     const bool pal = palette_on(p);
     for (int64_t rr = p.it0; rr < p.it0 + p.max_it; ++rr) {
         const uint32_t r = (uint32_t)rr;
+#ifdef EIK_DIAG
+        unsigned long long dgt0 = 0, dgt1 = 0;
+        int dgb = 0;
+        if (lead) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dgt0));
+#endif
         const int par = (int)(r & 1);
         const double *__restrict__ Pc = par ? p.P1 : p.P0;
         double *__restrict__ Pn = par ? p.P0 : p.P1;
@@ -1159,6 +1185,13 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
             ctl->iters = r + 1;
             ctl->sum += mg;
             if (mg > ctl->peak) ctl->peak = mg;
+#ifdef EIK_DIAG
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dgt1));
+            dgb = mg ? min(25, 63 - __clzll(mg)) : 0;
+            ctl->dg[0][dgb] += 1;
+            ctl->dg[1][dgb] += dgt1 - dgt0;
+            ctl->dg[3][dgb] += mg;
+#endif
         }
         // ---- phase A: one local solve per member, REM_MU members per lane in flight ----
         unsigned long long a_dec = 0;
@@ -1170,6 +1203,14 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
         const uint32_t sbeg = gb * seg, mend = min(m, sbeg + seg);
         const uint32_t wbase = sbeg + (threadIdx.x >> 5) * 32 * REM_MU, wstride = WPB * 32 * REM_MU;
 #endif
+#if REM_PREF
+        uint32_t nent[REM_MU];  // next iteration's list entries, loaded one iteration ahead
+#pragma unroll
+        for (int u = 0; u < REM_MU; ++u) {
+            const uint32_t i = wbase + u * 32 + lane;
+            nent[u] = i < mend ? __ldcg(ML + i) : 0u;
+        }
+#endif
         for (uint32_t i0 = wbase; i0 < mend; i0 += wstride) {
             uint32_t ent[REM_MU], rw[REM_MU], x[REM_MU];
             bool live[REM_MU];
@@ -1178,7 +1219,27 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
             for (int u = 0; u < REM_MU; ++u) {
                 const uint32_t i = i0 + u * 32 + lane;
                 live[u] = i < mend;
+#if REM_PREF
+                ent[u] = nent[u];
+                const uint32_t j = i + wstride;
+                nent[u] = j < mend ? __ldcg(ML + j) : 0u;
+#if REM_PREF > 1
+                if (j < mend) {  // warm L2 with the next member's rows (no registers held)
+                    const uint32_t cn = nent[u] & ~CARRY;
+                    const double *b = Pc + cn;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(b));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.dd + cn));
+                    if (cn >= nx) asm volatile("prefetch.global.L2 [%0];" ::"l"(b - nx));
+                    if (cn + nx < p.ncells) asm volatile("prefetch.global.L2 [%0];" ::"l"(b + nx));
+                    if (DIM == 3) {
+                        if (cn >= p.plane32) asm volatile("prefetch.global.L2 [%0];" ::"l"(b - p.plane32));
+                        if (cn + p.plane32 < p.ncells) asm volatile("prefetch.global.L2 [%0];" ::"l"(b + p.plane32));
+                    }
+                }
+#endif
+#else
                 ent[u] = live[u] ? __ldcg(ML + i) : 0u;
+#endif
             }
 #pragma unroll
             for (int u = 0; u < REM_MU; ++u) {
@@ -1247,6 +1308,13 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
             for (int q = 0; q < p.R; ++q) decs += __ldcg(&p.rank_ctl[q]->dsum[r % 3]);
         }
         if (p.slab) continue;  // the host reduces the counts and decides
+#ifdef EIK_DIAG
+        if (lead) {
+            unsigned long long dgt2;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dgt2));
+            ctl->dg[2][dgb] += dgt2 - dgt1;
+        }
+#endif
         if (lead) ctl->writes += decs;
         if (decs == 0) break;
         if (r + 1 >= (uint32_t)p.cap) {  // E/ifim.py:185-189
@@ -1430,7 +1498,7 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
 struct Layout {
     int64_t N;
-    uint32_t W, nwords;
+    uint32_t W, nwords, npos, nty4, ntt;
     size_t off_phi2, off_dd, off_bt, off_l0, off_l1;
     size_t off_r0, off_d0, off_d1, off_f, off_pidx, off_ptab, off_phash, off_pslot, off_pstate;
     size_t off_hist, off_ctl_u, off_ctl_r, off_kps, total;
@@ -1479,6 +1547,16 @@ int make_layout(const eik_geom *g, Layout &L)
     L.off_ctl_u = o; o += al(sizeof(Ctl));
     L.off_ctl_r = o; o += al(sizeof(Ctl));
     L.off_kps = o; o += al(2 * EIK_MAX_RANKS * sizeof(KP));
+    // member-list traversal (word_at): 3D groups of 4x4 rows, 2D groups of 16 rows, per x-word
+    if (g->ndim == 3) {
+        L.nty4 = (uint32_t)((g->ny + 3) / 4);
+        L.ntt = (uint32_t)((g->nz + 3) / 4);
+        L.npos = L.nty4 * L.ntt * 16 * L.W;
+    } else {
+        L.nty4 = 0;
+        L.ntt = (uint32_t)((g->ny + 15) / 16);
+        L.npos = L.ntt * 16 * L.W;
+    }
     L.total = o;
     return EIK_OK;
 }
@@ -1499,16 +1577,13 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const doub
     p.W = L.W; p.nwords = L.nwords; p.nrows = (uint32_t)(g->ny * g->nz);
     p.nx32 = (uint32_t)g->nx;
     p.plane32 = (uint32_t)(g->nx * g->ny);
+    p.ncells = (uint32_t)(g->nx * g->ny * g->nz);
     p.fnx = make_fastdiv((uint32_t)g->nx);
     p.fny = make_fastdiv((uint32_t)g->ny);
     p.fW = make_fastdiv(L.W);
-    if (g->ndim == 3) {
-        p.nty4 = (uint32_t)((g->ny + 3) / 4);
-        p.npos = p.nty4 * 4 * (uint32_t)((g->nz + 3) / 4) * 4 * L.W;
-    } else {
-        p.nty4 = 0;
-        p.npos = (uint32_t)((g->ny + 15) / 16) * 16 * L.W;
-    }
+    p.nty4 = L.nty4;
+    p.fnty4 = make_fastdiv(L.nty4 ? L.nty4 : 1);
+    p.npos = L.npos;
     p.dx = g->dx; p.dy = g->dy; p.delta = g->dx; p.tol = tol;
     p.slab = (g->flags & EIK_GEOM_SLAB) ? 1 : 0;
     p.it0 = 0;
@@ -2013,10 +2088,18 @@ int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t 
     out->build_ms = ev.ms(1, 2);
     out->rem_ms = ev.ms(2, 3);
     out->total_ms = ev.ms(0, 3);
-    if (getenv("EIK_DIAG_PRINT"))
+#ifdef EIK_DIAG
+    if (getenv("EIK_DIAG_PRINT")) {
         fprintf(stderr, "[eik diag] remedy member words %llu sectors %llu calls %llu\n",
                 (unsigned long long)c[1].nz_words, (unsigned long long)c[1].nz_sectors,
                 (unsigned long long)c[1].sum);
+        for (int k = 0; k < 26; ++k)
+            if (c[1].dg[0][k])
+                fprintf(stderr, "[eik diag] |R|~2^%2d rounds %6llu members %12llu  B %9.3f ms  A %9.3f ms  (%.2f/%.2f us per round)\n",
+                        k, c[1].dg[0][k], c[1].dg[3][k], c[1].dg[1][k] * 1e-6, c[1].dg[2][k] * 1e-6,
+                        c[1].dg[1][k] * 1e-3 / c[1].dg[0][k], c[1].dg[2][k] * 1e-3 / c[1].dg[0][k]);
+    }
+#endif
     if (history && history_cap > 0 && c[0].iters > 0) {
         const int64_t n = std::min<int64_t>((int64_t)c[0].iters, history_cap);
         CK(cudaMemcpy(history, b + L.off_hist, (size_t)n * 8, cudaMemcpyDeviceToHost));

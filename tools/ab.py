@@ -1,0 +1,62 @@
+"""A/B timing of engine variants on the same box: python tools/ab.py [--n 512] [--env K=V] VARIANT.so[:ENV=V] ...
+Each variant runs in its own process (checker n^3, 3 solves), alternating over 2 passes;
+prints the min device ms per phase."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+CHILD = r'''
+import sys, os, json
+sys.path.insert(0, sys.argv[1])
+from paper_2106_15869_b200 import _native
+_native.LIB = os.path.join(os.path.dirname(_native.LIB), sys.argv[2])
+import torch, paper_2106_15869_b200 as eik
+n = int(sys.argv[3]); kind = sys.argv[4]
+k = torch.arange(n, device="cuda") // max(1, n // 16)
+if kind == "checker":
+    F = torch.where(((k[None, None, :] + k[None, :, None] + k[:, None, None]) % 2) == 0, 1.0, 0.01).double()
+    seeds = [(n // 2, n // 2, n // 2)]
+else:
+    import numpy as np
+    F = torch.ones((n, n, n), dtype=torch.float64, device="cuda")
+    rng = np.random.default_rng(2106)
+    seeds = [tuple(int(v) for v in rng.integers(0, n, 3)) for _ in range(16)]
+best = None
+for r in range(3):
+    g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), float("inf"), dtype=torch.float64, device="cuda"),
+                   F, torch.zeros((n, n, n), dtype=torch.uint8, device="cuda"))
+    res = eik.solve_ifim(g, eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in seeds)))
+    d = res.stats.device_ms
+    if best is None or d["total"] < best["total"]:
+        best = dict(d)
+print("RESULT", json.dumps({"calls": res.stats.solver_calls, **best}))
+'''
+
+args = sys.argv[1:]
+n, kind = 512, "checker"
+if args and args[0] == "--n":
+    n, args = int(args[1]), args[2:]
+if args and args[0] == "--kind":
+    kind, args = args[1], args[2:]
+res = {v: [] for v in args}
+for p in range(2):
+    for v in args:
+        so, _, env = v.partition(":")
+        e = dict(os.environ)
+        if env:
+            k, _, val = env.partition("=")
+            e[k] = val
+        out = subprocess.run([sys.executable, "-c", CHILD, ROOT, so, str(n), kind], capture_output=True, text=True, env=e,
+                             timeout=300)
+        line = [l for l in out.stdout.splitlines() if l.startswith("RESULT")]
+        if not line:
+            print(v, "FAILED", out.stderr[-800:])
+            continue
+        res[v].append(json.loads(line[0][7:]))
+for v, rs in res.items():
+    if rs:
+        b = min(rs, key=lambda d: d["total"])
+        print(f"{v:40s} total {b['total']:8.2f} update {b['update']:7.2f} remedy {b['remedy']:8.2f}  "
+              f"(all totals {[round(d['total'], 1) for d in rs]}) calls {b['calls']}")
