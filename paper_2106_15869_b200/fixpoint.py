@@ -19,7 +19,8 @@ import torch
 
 from . import _native
 from .grid import seed_linear
-from .ifim import _check_tol, _DeviceGrid, _host_mark_sources, _ptr, geometry, resolve_workers, workspace
+from .ifim import (_check_tol, _DeviceGrid, _host_mark_sources, _HostResult, _ptr, geometry, resolve_workers,
+                   workspace)
 from .result import RunStats, SolverResult
 
 
@@ -35,18 +36,21 @@ def solve_fixpoint(grid, bc, tol: float = 1e-12, workers: int = 1, max_passes: i
     si = torch.as_tensor(idx, dtype=torch.int64, device=dg.device)
     sv = torch.as_tensor(val, dtype=torch.float64, device=dg.device)
     st = _native.Stats()
+    out = _HostResult(dg)
     rc = _native.lib().eik_solve_fixpoint(C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), _ptr(si),
                                           _ptr(sv), len(idx), float(tol), int(max_passes or 0), ws.ptr, ws.nbytes,
                                           C.byref(st), dg.stream)
+    phi = None
     if dg.host:
         _host_mark_sources(grid, idx)
-        dg.commit(phi=True)
+        phi = out.commit()
     _native.check(rc)
     stats = RunStats(iterations=int(st.iterations), solver_calls=int(st.solver_calls))
     stats.device_ms = {"total": float(st.total_ms)}
     stats.gpu_launches = int(st.gpu_launches)
+    if phi is None:
+        phi = grid.phi.copy() if isinstance(grid.phi, np.ndarray) else grid.phi.clone()
     stats.wall_time = time.perf_counter() - t0
-    phi = grid.phi.copy() if isinstance(grid.phi, np.ndarray) else grid.phi.clone()
     return SolverResult(phi=phi, stats=stats)
 
 

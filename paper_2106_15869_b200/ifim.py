@@ -120,6 +120,70 @@ def _copy_into(host_arr, dev_t):
             torch.cuda.current_stream(dev_t.device).synchronize()
 
 
+class _HostResult:
+    """SolverResult.phi for host grids (the reference returns grid.phi.copy()).
+
+    Large fields: the copy is allocated on a helper thread while the device
+    solves (the engine call releases the GIL).  A pinned caller array gets a
+    pinned copy (torch's caching host allocator reuses freed ones) filled by a
+    second device-to-host DMA, so no host memcpy is on the critical path; a
+    pageable caller array gets a first-touched pageable copy filled chunk by
+    chunk behind the device-to-host copy.
+    """
+
+    CHUNKS = 8
+    MIN_CELLS = 1 << 22
+
+    def __init__(self, dg):
+        self.dg, self.buf, self.thread = dg, None, None
+        phi = dg.grid.phi
+        self.pinned = isinstance(phi, torch.Tensor) and phi.is_pinned()
+        if dg.host and dg.phi.numel() >= self.MIN_CELLS:
+            import threading
+
+            def alloc():
+                if self.pinned:
+                    self.buf = torch.empty(tuple(phi.shape), dtype=torch.float64, pin_memory=True)
+                else:
+                    b = torch.empty(tuple(phi.shape), dtype=torch.float64)
+                    b.zero_()  # first touch off the critical path
+                    self.buf = b
+
+            self.thread = threading.Thread(target=alloc, daemon=True)
+            self.thread.start()
+
+    def commit(self):
+        """Device phi -> the caller's array and -> the result copy; returns the copy."""
+        dg, gphi = self.dg, self.dg.grid.phi
+        if self.thread is None:
+            dg.commit(phi=True)
+            return gphi.copy() if isinstance(gphi, np.ndarray) else gphi.clone()
+        self.thread.join()
+        buf = self.buf
+        host = torch.from_numpy(gphi) if isinstance(gphi, np.ndarray) else gphi
+        dev = dg.phi.reshape(host.shape)
+        stream = torch.cuda.current_stream(dg.device)
+        if self.pinned:
+            host.copy_(dev, non_blocking=True)
+            buf.copy_(dev, non_blocking=True)
+            stream.synchronize()
+        elif host.dim() >= 1 and host.shape[0] >= self.CHUNKS and host.is_pinned():
+            bounds = np.linspace(0, host.shape[0], self.CHUNKS + 1).astype(int)
+            events = []
+            for a, b in zip(bounds[:-1], bounds[1:]):
+                host[a:b].copy_(dev[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(stream)
+                events.append(ev)
+            for (a, b), ev in zip(zip(bounds[:-1], bounds[1:]), events):
+                ev.synchronize()
+                buf[a:b].copy_(host[a:b])  # overlaps the DMA of the next chunks
+        else:
+            dg.commit(phi=True)
+            buf.copy_(host)
+        return buf.numpy() if isinstance(gphi, np.ndarray) else buf
+
+
 def _host_mark_sources(grid, idx):
     """apply_boundary's state write (E/grid.py:215) on a host grid."""
     st = grid.state
@@ -360,12 +424,14 @@ def solve_ifim(grid, bc, tol: float = 1e-12, workers: int = 1) -> SolverResult:
     hcap = _history_cap(geom)
     hist = np.zeros(hcap, dtype=np.int64)
     st = _native.Stats()
+    out = _HostResult(dg)
     rc = _native.lib().eik_ifim_solve(
         C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), _ptr(si), _ptr(sv), len(idx), float(tol),
         ws.ptr, ws.nbytes, hist.ctypes.data_as(C.c_void_p), hcap, C.byref(st), dg.stream)
+    phi = None
     if dg.host:
         _host_mark_sources(grid, idx)
-        dg.commit(phi=True)
+        phi = out.commit()
     _native.check(rc)
     d = _stats_from(st)
     stats = RunStats(
@@ -383,6 +449,7 @@ def solve_ifim(grid, bc, tol: float = 1e-12, workers: int = 1) -> SolverResult:
     }
     stats.device_ms = {"update": d["upd_ms"], "build": d["build_ms"], "remedy": d["rem_ms"], "total": d["total_ms"]}
     stats.gpu_launches = d["gpu_launches"]
+    if phi is None:
+        phi = grid.phi.copy() if isinstance(grid.phi, np.ndarray) else grid.phi.clone()
     stats.wall_time = time.perf_counter() - t0
-    phi = grid.phi.copy() if isinstance(grid.phi, np.ndarray) else grid.phi.clone()
     return SolverResult(phi=phi, stats=stats)

@@ -265,3 +265,31 @@ def test_repeat_solves_reuse_workspace():
         res = eik.solve_ifim(g, eik.seed_point(g, (32, 32, 32), 0.0))
         outs.add((sha(res.phi), res.stats.solver_calls))
     assert len(outs) == 1
+
+
+def test_host_grid_large_result_copy_is_independent():
+    """Host grids >= 2^22 cells take the overlapped result copy (_HostResult): the caller's
+    phi and SolverResult.phi both hold the solved field and do not alias."""
+    n = 160
+    k = np.arange(n) // 10
+    F = np.where(((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2) == 0, 1.0, 0.01)
+    for pinned in (False, True):
+        phi = torch.full((n, n, n), np.inf, dtype=torch.float64)
+        st = torch.zeros((n, n, n), dtype=torch.uint8)
+        sp = torch.from_numpy(F)
+        if pinned:
+            phi, st, sp = phi.pin_memory(), st.pin_memory(), sp.pin_memory()
+        g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), phi, sp, st)
+        res = eik.solve_ifim(g, eik.seed_point(g, (80, 80, 80), 0.0))
+        dev = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), np.inf, dtype=torch.float64,
+                                                                    device="cuda"),
+                         torch.from_numpy(F).cuda(), torch.zeros((n, n, n), dtype=torch.uint8, device="cuda"))
+        ref = eik.solve_ifim(dev, eik.seed_point(dev, (80, 80, 80), 0.0))
+        assert torch.equal(res.phi, ref.phi.cpu()) and torch.equal(g.phi, ref.phi.cpu())
+        assert res.phi.data_ptr() != g.phi.data_ptr()
+        g.phi.fill_(0.0)
+        assert torch.equal(res.phi, ref.phi.cpu())
+    gn = eik.new_grid_3d(n, n, n, 1.0, speed=F)
+    res = eik.solve_ifim(gn, eik.seed_point(gn, (80, 80, 80), 0.0))
+    assert isinstance(res.phi, np.ndarray) and np.array_equal(res.phi, gn.phi) and not np.shares_memory(res.phi, gn.phi)
+    assert np.array_equal(res.phi, ref.phi.cpu().numpy())
