@@ -46,6 +46,80 @@ METRIC = "grid-node updates/sec (and wall-clock to convergence), 3D 512^3"
 UNIT = "node-updates/s"
 
 
+class Workload:
+    """One BASELINE.json config: speed field (device tensor), spacing, point seeds (i, j, k)."""
+
+    def __init__(self, name, n, h, F, seeds, desc):
+        self.name, self.n, self.h, self.F, self.seeds, self.desc = name, n, h, F, seeds, desc
+
+    def linear_seeds(self):
+        n = self.n
+        return [((k * n + j) * n + i, 0.0) for i, j, k in self.seeds]
+
+
+def cfg5_modes(n):
+    """cfg5 (SURVEY.md §8d / BASELINE.md): g = unit-variance sum of 32 Fourier modes with integer
+    wavevectors 0 < |k| <= 4 and uniform phases, 16 distinct seeds; all from default_rng(2106)."""
+    import itertools
+
+    rng = np.random.default_rng(2106)
+    ks = np.array([k for k in itertools.product(range(-4, 5), repeat=3) if 0 < sum(v * v for v in k) <= 16])
+    K = ks[rng.choice(len(ks), 32, replace=False)]
+    ph = rng.uniform(0.0, 2.0 * np.pi, 32)
+    seeds = []
+    while len(seeds) < 16:
+        s = tuple(int(v) for v in rng.integers(0, n, 3))
+        if s not in seeds:
+            seeds.append(s)
+    return K, ph, seeds
+
+
+def cfg5_speed(torch, dev, n):
+    """F = exp(0.5 g) on [0,1]^3 (h = 1/(n-1)), built plane-chunk by plane-chunk on the device."""
+    K, ph, seeds = cfg5_modes(n)
+    h = 1.0 / (n - 1)
+    x = torch.arange(n, dtype=torch.float64, device=dev) * h
+    F = torch.empty((n, n, n), dtype=torch.float64, device=dev)
+    zc = max(1, (1 << 26) // (n * n))
+    for z0 in range(0, n, zc):
+        z1 = min(n, z0 + zc)
+        g = torch.zeros((z1 - z0, n, n), dtype=torch.float64, device=dev)
+        for (kx, ky, kz), p in zip(K.tolist(), ph.tolist()):
+            a = 2 * np.pi * (kz * x[z0:z1])[:, None, None] + (2 * np.pi * ky * x)[None, :, None] + \
+                (2 * np.pi * kx * x + p)[None, None, :]
+            g += torch.cos(a)
+        F[z0:z1] = torch.exp(0.5 * 0.25 * g)  # sqrt(2/32) = 0.25: unit variance
+    return F, h, seeds
+
+
+def workload_desc(config, n):
+    if config == "cfg5":
+        return f"cfg5: 3D {n}^3 on [0,1]^3, F=exp(0.5 g) (32 Fourier modes |k|<=4, rng 2106), 16 seeds"
+    if config == "cfg3":
+        return f"cfg3: 3D {n}^3 F=1, h=1, 16 random seeds (rng 2106)"
+    return f"cfg4: 3D {n}^3 checkerboard 1:100 ({max(1, n // 16)}^3 blocks), h=1, seed (c,c,c)"
+
+
+def make_workload(torch, dev, config, n):
+    if config == "cfg5":
+        F, h, seeds = cfg5_speed(torch, dev, n)
+        return Workload("cfg5", n, h, F, seeds, workload_desc(config, n))
+    if config == "cfg3":
+        rng = np.random.default_rng(2106)
+        seeds = []
+        while len(seeds) < 16:
+            s = tuple(int(v) for v in rng.integers(0, n, 3))
+            if s not in seeds:
+                seeds.append(s)
+        return Workload("cfg3", n, 1.0, torch.ones((n, n, n), dtype=torch.float64, device=dev), seeds,
+                        workload_desc(config, n))
+    blk = max(1, n // 16)
+    kk = torch.arange(n, device=dev) // blk
+    F = torch.where(((kk[:, None, None] + kk[None, :, None] + kk[None, None, :]) % 2) == 0, 1.0, 0.01).double()
+    c = n // 2
+    return Workload("cfg4", n, 1.0, F, [(c, c, c)], workload_desc(config, n))
+
+
 def checker_speed_np(n: int, blk: int) -> np.ndarray:
     k = np.arange(n) // blk
     return np.where(((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2) == 0, 1.0, 0.01)
@@ -132,15 +206,18 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_sample(n: int, threads: int):
+def cpu_sample(n: int, threads: int, config: str = "cfg4"):
     """Oracle port (C, OpenMP) on the same workload family at n^3; returns (calls, seconds)."""
+    import torch
+
     from oracle import cpu
 
     cpu.build()
-    F = checker_speed_np(n, max(1, n // 16))
-    c = n // 2
+    w = make_workload(torch, torch.device("cpu"), config, n)
+    F = w.F.numpy()
+    sd = w.linear_seeds()
     t0 = time.perf_counter()
-    res = cpu.solve_ifim((n, n, n), 1.0, F, [(c * n + c) * n + c], [0.0], threads=threads)
+    res = cpu.solve_ifim((n, n, n), w.h, F, [c for c, _ in sd], [v for _, v in sd], threads=threads)
     dt = time.perf_counter() - t0
     return res.stats["solver_calls"], dt
 
@@ -159,10 +236,10 @@ def run_reference(args):
     threads = os.cpu_count() or 1
     n = args.cpu_size
     for _ in range(args.warmup):
-        cpu_sample(n, threads)
+        cpu_sample(n, threads, args.config)
     calls, secs = 0, 0.0
     for _ in range(args.steps):
-        c, s = cpu_sample(n, threads)
+        c, s = cpu_sample(n, threads, args.config)
         calls += c
         secs += s
     v = calls / secs
@@ -170,11 +247,11 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"cfg4 family: 3D {n}^3 checkerboard 1:100 ({max(1, n // 16)}^3 blocks), centre seed "
-                               f"(bounded CPU sample of the 512^3 workload)", "size": n, "parallelism": "host threads"},
+        "config": {"workload": workload_desc(args.config, args.size), "size": args.size,
+                   "parallelism": "host threads", "sample_size": n},
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"full solve_ifim of the {n}^3 checkerboard (same family), "
-                                   f"oracle/eik_oracle.c OpenMP x{threads}"},
+                         "sample": f"full solve_ifim of {workload_desc(args.config, n)} (same family, bounded "
+                                   f"sample of the {args.size}^3 workload), oracle/eik_oracle.c OpenMP x{threads}"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -188,13 +265,14 @@ class StepStats:
         self.launches, self.phase_ms = launches, phase_ms
 
 
-def make_single_step(eik, torch, dev, n, c, F):
+def make_single_step(eik, torch, dev, w):
     """One device-resident solve_ifim of the whole grid (inputs restored in the step)."""
+    n, F = w.n, w.F
     phi0 = torch.full((n, n, n), float("inf"), dtype=torch.float64, device=dev)
     st0 = torch.zeros((n, n, n), dtype=torch.uint8, device=dev)
     phi, st = torch.empty_like(phi0), torch.empty_like(st0)
-    g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), phi, F, st)
-    bc = eik.BoundaryCondition(((eik.CellIndex3D(c, c, c), 0.0),))
+    g = eik.Grid3D(n, n, n, w.h, (0.0, 0.0, 0.0), phi, F, st)
+    bc = eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in w.seeds))
 
     def step():
         phi.copy_(phi0)
@@ -209,17 +287,18 @@ def make_single_step(eik, torch, dev, n, c, F):
     return step
 
 
-def make_slab_step(torch, dev, n, c, F, world, rank):
+def make_slab_step(torch, dev, w, world, rank):
     """This rank's share of ONE z-sharded solve (paper_2106_15869_b200/slab.py protocol)."""
     from paper_2106_15869_b200.slab import SlabPartition, SlabSolver, ThreadComm, TorchDistComm
     from paper_2106_15869_b200.slab_gpu import SlabGpuEngine
 
+    n, F = w.n, w.F
     comm = TorchDistComm() if world > 1 else ThreadComm(0, ThreadComm.make_shared(1))
     z0, z1 = SlabPartition(n, world).bounds(rank)
     st0 = torch.zeros((n, n, n), dtype=torch.uint8, device=dev)
-    e = SlabGpuEngine((n, n, n), 1.0, F, st0, z0, z1, dev)
+    e = SlabGpuEngine((n, n, n), w.h, F, st0, z0, z1, dev)
     clean_state = e.state.clone()
-    seeds = [((c * n + c) * n + c, 0.0)]
+    seeds = w.linear_seeds()
     caps = (40 * 3 * n, 20 * 3 * n)
 
     def step():
@@ -252,19 +331,20 @@ def peer_slabs_possible(torch, dev, world, local):
     return bool(t.item())
 
 
-def make_peer_step(torch, dev, n, c, F, world, rank):
+def make_peer_step(torch, dev, w, world, rank):
     """This rank's share of ONE z-sharded solve in the fused peer-memory kernels
     (paper_2106_15869_b200/slab_peer.py): neighbour planes read over NVLink inside the
     persistent kernels, one device-side cross-rank barrier per iteration."""
     from paper_2106_15869_b200.slab import SlabPartition
     from paper_2106_15869_b200.slab_peer import DistributedSlabs
 
-    ds = DistributedSlabs((n, n, n), 1.0)
+    n = w.n
+    ds = DistributedSlabs((n, n, n), w.h)
     z0, z1 = SlabPartition(n, world).bounds(rank)
-    sp = F[z0:z1].contiguous()
+    sp = w.F[z0:z1].contiguous()
     st0 = torch.zeros((z1 - z0, n, n), dtype=torch.uint8, device=dev)
     st = torch.empty_like(st0)
-    seeds = [((c * n + c) * n + c, 0.0)]
+    seeds = w.linear_seeds()
 
     def step():
         st.copy_(st0)
@@ -292,19 +372,16 @@ def run_ours(args):
     import paper_2106_15869_b200 as eik
 
     n = args.size
-    blk = max(1, n // 16)
-    c = n // 2
-    workload = f"cfg4: 3D {n}^3 checkerboard 1:100 ({blk}^3 blocks), h=1, seed (c,c,c)"
-    kk = torch.arange(n, device=dev) // blk
-    F = torch.where(((kk[:, None, None] + kk[None, :, None] + kk[None, None, :]) % 2) == 0, 1.0, 0.01).double()
+    w = make_workload(torch, dev, args.config, n)
+    workload = w.desc
     slabs = world > 1 or args.slabs
     mode = "single"
     if world > 1 and not args.host_slabs and peer_slabs_possible(torch, dev, world, local):
-        step, mode = make_peer_step(torch, dev, n, c, F, world, rank), "peer"
+        step, mode = make_peer_step(torch, dev, w, world, rank), "peer"
     elif slabs:
-        step, mode = make_slab_step(torch, dev, n, c, F, world, rank), "host"
+        step, mode = make_slab_step(torch, dev, w, world, rank), "host"
     else:
-        step = make_single_step(eik, torch, dev, n, c, F)
+        step = make_single_step(eik, torch, dev, w)
 
     for _ in range(args.warmup):
         r = step()
@@ -353,10 +430,11 @@ def run_ours(args):
 
     out = None
     if rank == 0:
-        e2e = run_e2e(eik, torch, dev, n, blk, c, F.cpu().numpy(), calls, args) if not slabs else \
+        e2e = run_e2e(eik, torch, dev, w, calls, args) if not (slabs or args.no_e2e) else \
             {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
              "note": "e2e is measured by the single-GPU run through solve_ifim"}
-        cpu_calls, cpu_s = cpu_sample(args.cpu_size, os.cpu_count() or 1) if not args.no_cpu else (0, 0.0)
+        cpu_calls, cpu_s = cpu_sample(args.cpu_size, os.cpu_count() or 1, args.config) if not args.no_cpu \
+            else (0, 0.0)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -366,7 +444,7 @@ def run_ours(args):
                        "iterations": r.iterations, "peak_remedy": r.peak_remedy,
                        "parallelism": {"peer": f"z-slabs x{world} (peer-memory fused kernels)",
                                        "host": f"z-slabs x{world} (host-driven exchange)"}.get(mode, "single"),
-                       "l2": "inputs larger than L2 (phi 1 GiB fp64 per field at 512^3)",
+                       "l2": f"inputs larger than L2 (phi {n ** 3 * 8 / 2 ** 30:g} GiB fp64 per field at {n}^3)",
                        "phase_ms": r.phase_ms},
             "wall_clock_to_convergence_ms": ms / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -375,7 +453,7 @@ def run_ours(args):
                          "peak_source": peak_src},
             "cpu_baseline": {"value": (cpu_calls / cpu_s) if cpu_s else None, "unit": UNIT,
                              "cores": os.cpu_count() or 1, "kind": "port",
-                             "sample": f"full solve of the {args.cpu_size}^3 checkerboard (same family) with "
+                             "sample": f"full solve of {workload_desc(args.config, args.cpu_size)} (same family) with "
                                        f"oracle/eik_oracle.c, OpenMP x{os.cpu_count() or 1}, {cpu_s:.1f} s"},
             "e2e": e2e,
             "gpu_launches": launches,
@@ -391,13 +469,14 @@ def run_ours(args):
     return 0
 
 
-def run_e2e(eik, torch, dev, n, blk, c, F_host, calls, args):
+def run_e2e(eik, torch, dev, w, calls, args):
     """Same metric through solve_ifim with host buffers: H2D of phi/speed/state from pinned
     memory and D2H of phi inside each timed step."""
-    speed = torch.from_numpy(F_host).pin_memory()
+    n = w.n
+    speed = w.F.cpu().pin_memory()
     phi = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
     state = torch.empty((n, n, n), dtype=torch.uint8).pin_memory()
-    bc = eik.BoundaryCondition(((eik.CellIndex3D(c, c, c), 0.0),))
+    bc = eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in w.seeds))
     steps = max(1, min(args.steps, 3))
     warm = 2  # allocations: device grid, workspace, pinned result copies (cached by torch afterwards)
     tot = 0.0
@@ -405,7 +484,7 @@ def run_e2e(eik, torch, dev, n, blk, c, F_host, calls, args):
     for it in range(steps + warm):
         phi.fill_(float("inf"))
         state.zero_()
-        g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), phi, speed, state)
+        g = eik.Grid3D(n, n, n, w.h, (0.0, 0.0, 0.0), phi, speed, state)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = eik.solve_ifim(g, bc)
@@ -425,13 +504,18 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--size", type=int, default=512)
+    ap.add_argument("--size", type=int, default=None, help="grid edge (default 512; cfg5: 1024)")
+    ap.add_argument("--config", default="cfg4", choices=["cfg3", "cfg4", "cfg5"],
+                    help="BASELINE.json config (cfg4 = the headline 512^3 checkerboard)")
     ap.add_argument("--cpu-size", type=int, default=96)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--slabs", action="store_true", help="use the z-slab protocol even on one GPU")
     ap.add_argument("--host-slabs", action="store_true", help="N>1: host-driven NCCL slabs instead of peer memory")
     args = ap.parse_args()
+    if args.size is None:
+        args.size = 1024 if args.config == "cfg5" else (256 if args.config == "cfg3" else 512)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
