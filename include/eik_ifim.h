@@ -179,6 +179,9 @@ int eik_mr_run(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_be
                const double *const *speed, uint8_t *const *state, double tol, int64_t *history, int64_t history_cap,
                eik_stats *out, void *stream);
 
+/* Let `device` map `peer`'s memory (NVLink / NVSwitch P2P); single-process multi-GPU peer slabs. */
+int eik_peer_enable(int32_t device, int32_t peer);
+
 const char *eik_last_error(void);
 const char *eik_version(void);
 

@@ -32,7 +32,7 @@ EXPORTS = (
     "eik_remedy_export", "eik_remedy_step", "eik_ifim_solve", "eik_local_solve",
     "eik_last_error", "eik_version", "eik_workspace_offsets", "eik_slab_update_init", "eik_slab_update_iter",
     "eik_slab_apply_requests", "eik_slab_build", "eik_slab_remedy_round", "eik_solve_fixpoint",
-    "eik_max_residual", "eik_mr_prepare", "eik_mr_run",
+    "eik_max_residual", "eik_mr_prepare", "eik_mr_run", "eik_peer_enable",
 )
 
 
@@ -117,6 +117,7 @@ def lib():
     RP = C.POINTER(Rank)
     L.eik_mr_prepare.argtypes = [GP, C.c_int32, RP, C.c_int32, C.c_int32, P, P, P, P, i64, dbl, vp]
     L.eik_mr_run.argtypes = [GP, C.c_int32, RP, C.c_int32, C.c_int32, P, P, dbl, P, i64, SP, vp]
+    L.eik_peer_enable.argtypes = [C.c_int32, C.c_int32]
     L.eik_last_error.restype = C.c_char_p
     L.eik_version.restype = C.c_char_p
     _lib = L

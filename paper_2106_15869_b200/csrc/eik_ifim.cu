@@ -2253,6 +2253,25 @@ static int mr_setup(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t
     return EIK_OK;
 }
 
+int eik_peer_enable(int32_t device, int32_t peer)
+{
+    if (device == peer) return EIK_OK;
+    int can = 0;
+    CK(cudaDeviceCanAccessPeer(&can, device, peer));
+    if (!can) return fail(EIK_EINVAL, "device %d cannot map device %d's memory (no NVLink/P2P path)", device, peer);
+    int cur = 0;
+    CK(cudaGetDevice(&cur));
+    CK(cudaSetDevice(device));
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        (void)cudaGetLastError();
+        e = cudaSuccess;
+    }
+    cudaSetDevice(cur);
+    if (e != cudaSuccess) return fail(EIK_ECUDA, "enable peer access %d -> %d: %s", device, peer, cudaGetErrorString(e));
+    return EIK_OK;
+}
+
 int eik_mr_prepare(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_begin, int32_t r_end,
                    const double *const *speed, uint8_t *const *state, const int64_t *seeds, const double *seed_val,
                    int64_t nseeds, double tol, void *stream)

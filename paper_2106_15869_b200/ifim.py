@@ -409,12 +409,24 @@ def ifim_remedy_step(grid, remedy: RemedySet, tol: float = 1e-12, workers: int =
     return stats
 
 
-def solve_ifim(grid, bc, tol: float = 1e-12, workers: int = 1) -> SolverResult:
-    """Update step + build + remedy, device-resident (E/ifim.py:221-235)."""
+def solve_ifim(grid, bc, tol: float = 1e-12, workers: int = 1, devices=None) -> SolverResult:
+    """Update step + build + remedy, device-resident (E/ifim.py:221-235).
+
+    ``devices`` (or EIKONAL_DEVICES): a GPU count or a list of CUDA indices; more than one
+    shards a Grid3D into z-slabs solved by the peer-memory kernels (slab_peer.solve_multi),
+    with results and statistics identical to the single-device solve.
+    """
     t0 = time.perf_counter()
     _check_tol(tol)
     resolve_workers(workers)
+    from .slab_peer import resolve_devices, solve_multi
+
+    devs = resolve_devices(devices)
     idx, val = seed_linear(grid, bc)
+    if devs is not None:
+        stats, phi = solve_multi(grid, idx, val, tol, devs)
+        stats.wall_time = time.perf_counter() - t0
+        return SolverResult(phi=phi, stats=stats)
     dg = _DeviceGrid(grid)
     geom = geometry(grid)
     ws = workspace(geom, dg.device)

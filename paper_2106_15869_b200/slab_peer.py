@@ -18,6 +18,8 @@ Results and every RunStats integer are identical to the single-device solve.
 from __future__ import annotations
 
 import ctypes as C
+import os
+import threading
 
 import numpy as np
 import torch
@@ -150,3 +152,133 @@ class DistributedSlabs:
         _native.check(lib.eik_mr_run(C.byref(g), self.R, self.ranks, self.rank, self.rank + 1, spp, stp, float(tol),
                                      hist.ctypes.data_as(C.c_void_p), hcap, C.byref(out), stream))
         return self.phi, _stats(out, hist)
+
+
+# ---------------------------------------------------------------------------
+# solve_ifim(..., devices=...): one process, several GPUs
+# ---------------------------------------------------------------------------
+
+def resolve_devices(devices):
+    """``devices`` (int count or list of CUDA indices) or EIKONAL_DEVICES -> list of devices per
+    z-slab rank, or None for the single-device path.  A device may appear more than once (its
+    ranks then share one launch); ranks on one device must be contiguous."""
+    if devices is None:
+        env = os.environ.get("EIKONAL_DEVICES", "").strip()
+        if not env:
+            return None
+        devices = int(env) if env.isdigit() else [int(v) for v in env.split(",") if v.strip()]
+    if isinstance(devices, (int, np.integer)) and not isinstance(devices, bool):
+        if devices < 1:
+            raise ValueError(f"devices must be >= 1, got {devices}")
+        if devices > torch.cuda.device_count():
+            raise ValueError(f"devices={devices} but only {torch.cuda.device_count()} CUDA devices are visible")
+        devices = list(range(int(devices)))
+    devices = [int(d) for d in devices]
+    if not devices:
+        raise ValueError("devices is empty")
+    n = torch.cuda.device_count()
+    for d in devices:
+        if not 0 <= d < n:
+            raise ValueError(f"CUDA device {d} is not visible ({n} devices)")
+    seen = []
+    for d in devices:
+        if seen and d != seen[-1] and d in seen:
+            raise ValueError(f"ranks on one device must be contiguous, got {devices}")
+        seen.append(d)
+    return devices if len(devices) > 1 else None
+
+
+def solve_multi(grid, idx, val, tol, devices):
+    """Peer-slab solve of a Grid3D over ``devices`` (one z-slab rank per entry).  Mutates
+    grid.phi / grid.state like the single-device solve; returns (RunStats, phi copy)."""
+    from .grid import CellState
+
+    if len(grid.phi.shape) != 3:
+        raise ValueError("a multi-device solve shards z-slabs of a 3D grid (Grid3D)")
+    nz, ny, nx = (int(v) for v in grid.phi.shape)
+    R = len(devices)
+    part = SlabPartition(nz, R)
+    bounds = [part.bounds(r) for r in range(R)]
+    h = float(grid.dx)
+    if not (grid.dx == grid.dy == grid.dz):
+        raise ValueError("3D grids require dx == dy == dz")
+
+    def src(a):
+        return a if isinstance(a, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(a))
+
+    phi_src, sp_src, st_src = src(grid.phi), src(grid.speed), src(grid.state)
+    lib = _native.lib()
+    for a in sorted(set(devices)):
+        for b in sorted(set(devices)):
+            if a != b:
+                _native.check(lib.eik_peer_enable(a, b))
+    phis, sps, sts, wss = [], [], [], []
+    for q, (z0, z1) in enumerate(bounds):
+        dev = torch.device("cuda", devices[q])
+        phis.append(phi_src[z0:z1].to(dev, torch.float64).contiguous())
+        sps.append(sp_src[z0:z1].to(dev, torch.float64).contiguous())
+        sts.append(st_src[z0:z1].to(dev, torch.uint8).contiguous().clone())
+        wss.append(torch.empty(_ws_bytes(nx, ny, z1 - z0, h), dtype=torch.uint8, device=dev))
+    ranks = (_native.Rank * R)(*[_native.Rank(t.data_ptr(), w.data_ptr(), z1 - z0)
+                                  for t, w, (z0, z1) in zip(phis, wss, bounds)])
+    groups = []  # (device, r_begin, r_end)
+    for q, d in enumerate(devices):
+        if groups and groups[-1][0] == d:
+            groups[-1][2] = q + 1
+        else:
+            groups.append([d, q, q + 1])
+    g = _geom((nz, ny, nx), h)
+    hcap = 40 * (nx + ny + nz) + 2
+    outs, hists, errs = {}, {}, {}
+    seeds = {}
+    for d, rb, re in groups:
+        dev = torch.device("cuda", d)
+        with torch.cuda.device(dev):
+            seeds[d] = (torch.as_tensor(idx, dtype=torch.int64, device=dev),
+                        torch.as_tensor(val, dtype=torch.float64, device=dev))
+            spp = (C.c_void_p * (re - rb))(*[t.data_ptr() for t in sps[rb:re]])
+            stp = (C.c_void_p * (re - rb))(*[t.data_ptr() for t in sts[rb:re]])
+            stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+            _native.check(lib.eik_mr_prepare(C.byref(g), R, ranks, rb, re, spp, stp, _p(seeds[d][0]),
+                                             _p(seeds[d][1]), len(idx), float(tol), stream))
+
+    def run(d, rb, re):
+        dev = torch.device("cuda", d)
+        try:
+            with torch.cuda.device(dev):
+                spp = (C.c_void_p * (re - rb))(*[t.data_ptr() for t in sps[rb:re]])
+                stp = (C.c_void_p * (re - rb))(*[t.data_ptr() for t in sts[rb:re]])
+                stream = C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+                hist = np.zeros(hcap, dtype=np.int64)
+                out = _native.Stats()
+                rc = lib.eik_mr_run(C.byref(g), R, ranks, rb, re, spp, stp, float(tol),
+                                    hist.ctypes.data_as(C.c_void_p), hcap, C.byref(out), stream)
+                outs[d], hists[d] = out, hist
+                if rc:
+                    errs[d] = (rc, lib.eik_last_error().decode(errors="replace"))
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs[d] = (-1, repr(e))
+
+    threads = [threading.Thread(target=run, args=tuple(gr)) for gr in groups]
+    for t in threads:  # every device's persistent kernels must be resident together (cross-rank barrier)
+        t.start()
+    for t in threads:
+        t.join()
+    if errs:
+        rc, msg = next(iter(errs.values()))
+        if rc == 2:
+            raise RuntimeError(msg)
+        raise RuntimeError(f"multi-device solve failed: {msg}")
+    d0 = groups[0][0]
+    stats = _stats(outs[d0], hists[d0])
+    # write back (in place, like the single-device solve)
+    for q, (z0, z1) in enumerate(bounds):
+        if isinstance(grid.phi, torch.Tensor):
+            grid.phi[z0:z1].copy_(phis[q].to(grid.phi.device))
+        else:
+            grid.phi[z0:z1] = phis[q].cpu().numpy()
+    flat = grid.state.reshape(-1)
+    for c in idx:
+        flat[c] = CellState.SOURCE
+    phi = grid.phi.copy() if isinstance(grid.phi, np.ndarray) else grid.phi.clone()
+    return stats, phi

@@ -125,3 +125,22 @@ def test_remedy_set_host_side():
     rs2 = eik.RemedySet(member=member.copy(), cells=[3, 7])
     rs2._drain()
     assert len(rs2) == 0 and not rs2.member.any()
+
+
+def test_resolve_devices(monkeypatch):
+    """devices= / EIKONAL_DEVICES selection for the multi-device z-slab solve."""
+    from paper_2106_15869_b200.slab_peer import resolve_devices
+
+    monkeypatch.delenv("EIKONAL_DEVICES", raising=False)
+    assert resolve_devices(None) is None
+    monkeypatch.setattr(torch.cuda, "device_count", lambda: 4)
+    assert resolve_devices(1) is None and resolve_devices([2]) is None
+    assert resolve_devices(3) == [0, 1, 2]
+    assert resolve_devices([1, 1, 3]) == [1, 1, 3]
+    for bad in (0, 5, [0, 1, 0], [4], []):
+        with pytest.raises(ValueError):
+            resolve_devices(bad)
+    monkeypatch.setenv("EIKONAL_DEVICES", "2")
+    assert resolve_devices(None) == [0, 1]
+    monkeypatch.setenv("EIKONAL_DEVICES", "0,0,2")
+    assert resolve_devices(None) == [0, 0, 2]

@@ -78,3 +78,39 @@ def test_distributed_peer_slabs_symmetric_memory():
                        capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "bit-identical=True" in r.stdout
+
+
+@pytest.mark.parametrize("devices", [[0, 0], [0, 0, 0]])
+def test_solve_ifim_devices_kwarg(devices):
+    """solve_ifim(..., devices=...) shards a Grid3D over z-slab ranks; several ranks on one
+    device share a launch.  Field, state and stats equal the single-device solve."""
+    shape, h, F, state, seeds = problem("walls")
+    nz, ny, nx = shape
+    bc = eik.BoundaryCondition(tuple((eik.CellIndex3D(c % nx, (c // nx) % ny, c // (nx * ny)), v) for c, v in seeds))
+    g1 = eik.new_grid_3d(nx, ny, nz, h, speed=F)
+    ref = eik.solve_ifim(g1, bc)
+    g2 = eik.new_grid_3d(nx, ny, nz, h, speed=F)
+    res = eik.solve_ifim(g2, bc, devices=devices)
+    assert np.array_equal(res.phi.view(np.uint64), ref.phi.view(np.uint64))
+    assert np.array_equal(g2.phi.view(np.uint64), g1.phi.view(np.uint64)) and np.array_equal(g2.state, g1.state)
+    a, b = res.stats, ref.stats
+    assert (a.iterations, a.solver_calls, a.peak_active, a.peak_remedy, a.active_history) == \
+        (b.iterations, b.solver_calls, b.peak_active, b.peak_remedy, b.active_history)
+
+
+def test_devices_env_and_2d_rejected(monkeypatch):
+    shape, h, F, state, seeds = problem("checker")
+    nz, ny, nx = shape
+    dev = torch.device("cuda:0")
+    mk = lambda: eik.Grid3D(nx, ny, nz, h, (0.0, 0.0, 0.0), torch.full(shape, np.inf, dtype=torch.float64, device=dev),
+                            torch.as_tensor(F, device=dev), torch.as_tensor(state, device=dev))
+    bc = eik.BoundaryCondition(tuple((eik.CellIndex3D(c % nx, (c // nx) % ny, c // (nx * ny)), v) for c, v in seeds))
+    g1 = mk()
+    ref = eik.solve_ifim(g1, bc)
+    monkeypatch.setenv("EIKONAL_DEVICES", "0,0,0,0")
+    g2 = mk()
+    res = eik.solve_ifim(g2, bc)
+    assert torch.equal(res.phi, ref.phi) and res.stats.solver_calls == ref.stats.solver_calls
+    g2d = eik.new_grid(16, 16, 1.0, 1.0)
+    with pytest.raises(ValueError, match="3D"):
+        eik.solve_ifim(g2d, eik.seed_point(g2d, (3, 3), 0.0))
