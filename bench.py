@@ -265,10 +265,10 @@ class StepStats:
         self.launches, self.phase_ms = launches, phase_ms
 
 
-def make_single_step(eik, torch, dev, w):
+def make_single_step(eik, torch, dev, w, dtype):
     """One device-resident solve_ifim of the whole grid (inputs restored in the step)."""
-    n, F = w.n, w.F
-    phi0 = torch.full((n, n, n), float("inf"), dtype=torch.float64, device=dev)
+    n, F = w.n, w.F.to(dtype)
+    phi0 = torch.full((n, n, n), float("inf"), dtype=dtype, device=dev)
     st0 = torch.zeros((n, n, n), dtype=torch.uint8, device=dev)
     phi, st = torch.empty_like(phi0), torch.empty_like(st0)
     g = eik.Grid3D(n, n, n, w.h, (0.0, 0.0, 0.0), phi, F, st)
@@ -374,6 +374,10 @@ def run_ours(args):
     n = args.size
     w = make_workload(torch, dev, args.config, n)
     workload = w.desc
+    rdt = torch.float32 if args.dtype == "f32" else torch.float64
+    rsize = 4 if args.dtype == "f32" else 8
+    if args.dtype == "f32" and (world > 1 or args.slabs):
+        raise SystemExit("the float32 perf mode is single-device")
     slabs = world > 1 or args.slabs
     mode = "single"
     if world > 1 and not args.host_slabs and peer_slabs_possible(torch, dev, world, local):
@@ -381,7 +385,7 @@ def run_ours(args):
     elif slabs:
         step, mode = make_slab_step(torch, dev, w, world, rank), "host"
     else:
-        step = make_single_step(eik, torch, dev, w)
+        step = make_single_step(eik, torch, dev, w, rdt)
 
     for _ in range(args.warmup):
         r = step()
@@ -420,17 +424,17 @@ def run_ours(args):
     # 8 B x (2 x solver_calls + phi_writes) of the remedy phase) / its CUDA-event duration.
     # Peer mode: the counts are global and the ranks run in lockstep, so the figure is the
     # aggregate over the ranks against the aggregate peak.
-    alg_bytes = 8.0 * (2 * r.rem_calls + r.rem_writes)
+    alg_bytes = float(rsize) * (2 * r.rem_calls + r.rem_writes)
     rem_s = statistics.median(rem_ms) / 1e3
     peak, peak_src = hbm_peak()
     if mode == "peer":
         peak, peak_src = peak * world, peak_src + f" x {world} ranks"
     achieved = alg_bytes / rem_s / 1e9 if rem_s > 0 else None
-    traffic = traffic_from_profiles(workload) if not slabs else None
+    traffic = traffic_from_profiles(workload) if not slabs and args.dtype == "f64" else None
 
     out = None
     if rank == 0:
-        e2e = run_e2e(eik, torch, dev, w, calls, args) if not (slabs or args.no_e2e) else \
+        e2e = run_e2e(eik, torch, dev, w, calls, args, rdt) if not (slabs or args.no_e2e) else \
             {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
              "note": "e2e is measured by the single-GPU run through solve_ifim"}
         cpu_calls, cpu_s = cpu_sample(args.cpu_size, os.cpu_count() or 1, args.config) if not args.no_cpu \
@@ -439,7 +443,7 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if slabs else "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": workload, "size": n, "solver_calls_per_step": calls,
                        "iterations": r.iterations, "peak_remedy": r.peak_remedy,
                        "parallelism": {"peer": f"z-slabs x{world} (peer-memory fused kernels)",
@@ -469,12 +473,12 @@ def run_ours(args):
     return 0
 
 
-def run_e2e(eik, torch, dev, w, calls, args):
+def run_e2e(eik, torch, dev, w, calls, args, rdt):
     """Same metric through solve_ifim with host buffers: H2D of phi/speed/state from pinned
     memory and D2H of phi inside each timed step."""
     n = w.n
-    speed = w.F.cpu().pin_memory()
-    phi = torch.empty((n, n, n), dtype=torch.float64).pin_memory()
+    speed = w.F.to(rdt).cpu().pin_memory()
+    phi = torch.empty((n, n, n), dtype=rdt).pin_memory()
     state = torch.empty((n, n, n), dtype=torch.uint8).pin_memory()
     bc = eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in w.seeds))
     steps = max(1, min(args.steps, 3))
@@ -495,8 +499,9 @@ def run_e2e(eik, torch, dev, w, calls, args):
     N = n ** 3
     # D2H: phi into the caller's array (in-place API) and into SolverResult.phi (the
     # reference returns grid.phi.copy()), both DMA from the device
-    return {"value": calls * steps / tot, "unit": UNIT, "h2d_bytes_per_step": N * (8 + 8 + 1),
-            "d2h_bytes_per_step": 2 * N * 8, "steps": steps, "ms_per_step": tot / steps * 1e3}
+    rs = phi.element_size()
+    return {"value": calls * steps / tot, "unit": UNIT, "h2d_bytes_per_step": N * (rs + rs + 1),
+            "d2h_bytes_per_step": 2 * N * rs, "steps": steps, "ms_per_step": tot / steps * 1e3}
 
 
 def main():
@@ -511,6 +516,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
+                    help="f64 = parity mode (default, bit-exact); f32 = perf mode (max-rel 1e-5)")
     ap.add_argument("--slabs", action="store_true", help="use the z-slab protocol even on one GPU")
     ap.add_argument("--host-slabs", action="store_true", help="N>1: host-driven NCCL slabs instead of peer memory")
     args = ap.parse_args()

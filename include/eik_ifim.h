@@ -43,7 +43,8 @@ extern "C" {
 #define EIK_ECUDA 3
 #define EIK_ENCCL 4
 
-#define EIK_F64 0
+#define EIK_F64 0 /* libeik_ifim.so: float64 fields, bit-exact with the reference */
+#define EIK_F32 1 /* libeik_ifim_f32.so: float32 fields (perf mode), names suffixed _f32 */
 
 #define EIK_GEOM_SLAB 1 /* flags: local z-slab of a sharded 3D grid, planes 0 and nz-1 are ghosts */
 
@@ -184,6 +185,36 @@ int eik_peer_enable(int32_t device, int32_t peer);
 
 const char *eik_last_error(void);
 const char *eik_version(void);
+
+/* ---- float32 perf mode (libeik_ifim_f32.so) ----
+ * Same semantics and statistics definitions with float32 phi / speed (geometry
+ * dtype EIK_F32, tol compared in float32).  The float32 solve is a different
+ * rounding of the same algorithm: its phi is checked against the float64 solve
+ * at max-rel 1e-5, its counts are its own.  Single device. */
+int eik_workspace_size_f32(const eik_geom *g, size_t *bytes);
+int eik_ifim_update_step_f32(const eik_geom *g, float *phi, const float *speed, uint8_t *state,
+                             const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
+                             void *workspace, size_t workspace_bytes, int64_t *history, int64_t history_cap,
+                             eik_stats *out, void *stream);
+int eik_build_remedy_f32(const eik_geom *g, const float *phi, const float *speed, const uint8_t *state, double tol,
+                         void *workspace, size_t workspace_bytes, eik_stats *out, void *stream);
+int eik_remedy_load_f32(const eik_geom *g, const uint8_t *member, const uint8_t *state, void *workspace,
+                        size_t workspace_bytes, int64_t *count, void *stream);
+int eik_remedy_export_f32(const eik_geom *g, void *workspace, size_t workspace_bytes, uint8_t *member, void *stream);
+int eik_remedy_step_f32(const eik_geom *g, float *phi, const float *speed, const uint8_t *state, double tol,
+                        void *workspace, size_t workspace_bytes, eik_stats *out, void *stream);
+int eik_ifim_solve_f32(const eik_geom *g, float *phi, const float *speed, uint8_t *state, const int64_t *seed_idx,
+                       const double *seed_val, int64_t nseeds, double tol, void *workspace, size_t workspace_bytes,
+                       int64_t *history, int64_t history_cap, eik_stats *out, void *stream);
+int eik_solve_fixpoint_f32(const eik_geom *g, float *phi, const float *speed, uint8_t *state,
+                           const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
+                           int64_t max_passes, void *workspace, size_t workspace_bytes, eik_stats *out, void *stream);
+int eik_max_residual_f32(const eik_geom *g, const float *phi, const float *speed, const uint8_t *state,
+                         void *workspace, size_t workspace_bytes, double *out, void *stream);
+int eik_local_solve_f32(int kind, const float *a, const float *b, const float *c, const float *f, double dx,
+                        double dy, float *out, int64_t n, void *stream);
+const char *eik_last_error_f32(void);
+const char *eik_version_f32(void);
 
 #ifdef __cplusplus
 }

@@ -16,6 +16,8 @@ ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "eik_ifim.cu")
 HDR = os.path.join(ROOT, "include", "eik_ifim.h")
 LIB = os.path.join(HERE, "libeik_ifim.so")
+LIB32 = os.path.join(HERE, "libeik_ifim_f32.so")  # float32 perf mode (-DEIK_SINGLE=1, names suffixed _f32)
+EIK_F64, EIK_F32 = 0, 1
 
 EIK_OK, EIK_EINVAL, EIK_ECAP, EIK_ECUDA, EIK_ENCCL = 0, 1, 2, 3, 4
 
@@ -44,14 +46,16 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile csrc/eik_ifim.cu into paper_2106_15869_b200/libeik_ifim.so."""
-    stale = (not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(SRC), os.path.getmtime(HDR)))
-    if force or stale:
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp", SRC]
-        if verbose:
-            cmd.insert(1, "-Xptxas=-v")
-        subprocess.check_call(cmd)
-        os.replace(LIB + ".tmp", LIB)
+    """Compile csrc/eik_ifim.cu into paper_2106_15869_b200/libeik_ifim.so (float64) and
+    libeik_ifim_f32.so (float32 perf mode)."""
+    src_t = max(os.path.getmtime(SRC), os.path.getmtime(HDR))
+    for out, extra in ((LIB, []), (LIB32, ["-DEIK_SINGLE=1"])):
+        if force or not os.path.exists(out) or os.path.getmtime(out) < src_t:
+            cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp", SRC]
+            if verbose:
+                cmd.insert(1, "-Xptxas=-v")
+            subprocess.check_call(cmd)
+            os.replace(out + ".tmp", out)
     return LIB
 
 
@@ -84,12 +88,34 @@ class Stats(C.Structure):
                 for k, t in self._fields_}
 
 
+EXPORTS_F32 = (
+    "eik_workspace_size_f32", "eik_ifim_update_step_f32", "eik_build_remedy_f32", "eik_remedy_load_f32",
+    "eik_remedy_export_f32", "eik_remedy_step_f32", "eik_ifim_solve_f32", "eik_solve_fixpoint_f32",
+    "eik_max_residual_f32", "eik_local_solve_f32", "eik_last_error_f32", "eik_version_f32",
+)
+
 _lib = None
+_lib32 = None
+_last_dtype = EIK_F64
 
 
-def lib():
-    """The loaded engine; raises if it was not built (no CPU fallback)."""
-    global _lib
+class _Suffixed:
+    """The float32 library seen under the float64 entry-point names."""
+
+    def __init__(self, cdll):
+        self._l = cdll
+
+    def __getattr__(self, name):
+        return getattr(self._l, name + "_f32")
+
+
+def lib(dtype: int = EIK_F64):
+    """The loaded engine (float64, or the float32 perf-mode library for dtype EIK_F32);
+    raises if it was not built (no CPU fallback)."""
+    global _lib, _last_dtype
+    _last_dtype = dtype  # check() reads the error text of the library used last
+    if dtype == EIK_F32:
+        return _lib_f32()
     if _lib is not None:
         return _lib
     if not os.path.exists(LIB):
@@ -124,11 +150,36 @@ def lib():
     return L
 
 
-def check(rc: int) -> None:
+def _lib_f32():
+    global _lib32
+    if _lib32 is not None:
+        return _lib32
+    if not os.path.exists(LIB32):
+        raise RuntimeError(f"B200 float32 engine not built: {LIB32} is missing (run __graft_entry__.build())")
+    L = C.CDLL(LIB32)
+    P, i64, dbl, vp = C.c_void_p, C.c_int64, C.c_double, C.c_void_p
+    GP, SP = C.POINTER(Geom), C.POINTER(Stats)
+    L.eik_workspace_size_f32.argtypes = [GP, C.POINTER(C.c_size_t)]
+    L.eik_ifim_update_step_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]
+    L.eik_build_remedy_f32.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, SP, vp]
+    L.eik_remedy_load_f32.argtypes = [GP, P, P, P, C.c_size_t, C.POINTER(i64), vp]
+    L.eik_remedy_export_f32.argtypes = [GP, P, C.c_size_t, P, vp]
+    L.eik_remedy_step_f32.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, SP, vp]
+    L.eik_ifim_solve_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]
+    L.eik_solve_fixpoint_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, i64, P, C.c_size_t, SP, vp]
+    L.eik_max_residual_f32.argtypes = [GP, P, P, P, P, C.c_size_t, C.POINTER(dbl), vp]
+    L.eik_local_solve_f32.argtypes = [C.c_int, P, P, P, P, dbl, dbl, P, i64, vp]
+    L.eik_last_error_f32.restype = C.c_char_p
+    L.eik_version_f32.restype = C.c_char_p
+    _lib32 = _Suffixed(L)
+    return _lib32
+
+
+def check(rc: int, dtype: int | None = None) -> None:
     """Map a C-ABI status to the reference's exception types."""
     if rc == EIK_OK:
         return
-    msg = lib().eik_last_error().decode(errors="replace")
+    msg = lib(_last_dtype if dtype is None else dtype).eik_last_error().decode(errors="replace")
     if rc == EIK_EINVAL:
         raise ValueError(msg)
     raise RuntimeError(msg)

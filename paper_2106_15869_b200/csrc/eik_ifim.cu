@@ -45,6 +45,21 @@
 
 #include "eik_ifim.h"
 
+// Field precision: float64 (parity mode, libeik_ifim.so) or float32 (perf mode,
+// libeik_ifim_f32.so: -DEIK_SINGLE=1, exported names carry the _f32 suffix).
+#ifndef EIK_SINGLE
+#define EIK_SINGLE 0
+#endif
+#if EIK_SINGLE
+typedef float real_t;
+#define EIK_FN(name) name##_f32
+#define EIK_DTYPE EIK_F32
+#else
+typedef double real_t;
+#define EIK_FN(name) name
+#define EIK_DTYPE EIK_F64
+#endif
+
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
@@ -54,8 +69,24 @@ constexpr uint8_t ST_SOURCE = 2, ST_BLOCKED = 4;  // E/grid.py:21-26
 enum { SOL_U2 = 0, SOL_A2 = 1, SOL_U3 = 2 };
 
 // E/_kernels.py:18 (math.sqrt(2.0)) and E/local_solver.py:28
-constexpr double kSqrt2 = 1.4142135623730951;
-#define DISC_CLAMP 1e-12
+constexpr real_t kSqrt2 = (real_t)1.4142135623730951;
+constexpr real_t DISC_CLAMP = (real_t)1e-12;
+constexpr real_t R_HALF = (real_t)0.5, R_ONE = (real_t)1.0, R_TWO = (real_t)2.0, R_THREE = (real_t)3.0, R_ZERO = (real_t)0.0;
+
+// IEEE bits of a non-negative value, ordered like the value (atomicMax reductions, palette keys)
+#if EIK_SINGLE
+__device__ __forceinline__ unsigned long long bits_of(float x) { return (unsigned long long)__float_as_uint(x); }
+#else
+__device__ __forceinline__ unsigned long long bits_of(double x) { return (unsigned long long)__double_as_longlong(x); }
+#endif
+__device__ __forceinline__ real_t real_of_bits(unsigned long long b)
+{
+#if EIK_SINGLE
+    return __uint_as_float((unsigned)b);
+#else
+    return __longlong_as_double((long long)b);
+#endif
+}
 
 struct Ctl {
     unsigned bar_count;
@@ -87,7 +118,7 @@ constexpr int EIK_MAX_RANKS = 16;
 // of phi and of the decrease bitmap directly and activates cells on its
 // boundary plane with atomics on its touched bitmap and next worklist.
 struct Peer {
-    double *P0, *P1;
+    real_t *P0, *P1;
     uint32_t *Bt, *L0, *L1, *D0b, *D1b;
     Ctl *ctl;
     uint32_t nz;     // its owned planes
@@ -123,16 +154,16 @@ struct KP {
     uint32_t nx32, plane32;  // cell indices are < 2^31 (make_layout)
     uint32_t npos, nty4;     // remedy member-list traversal: positions (padded bricks), 4-row tiles in y
     FastDiv fnx, fny, fW, fnty4;
-    double dx, dy, delta, tol;
+    real_t dx, dy, delta, tol;
     int32_t slab;            // 1: z-slab of a sharded 3D grid, planes 0 and nz-1 are ghosts
     int32_t pad1;
     int64_t it0, max_it;     // iteration window of one persistent launch (slab mode: one step)
-    double *P0, *P1;         // P0 = caller phi, P1 = workspace copy
-    const double *F;         // speed
-    double *dd;              // delta / F (uniform solvers)
+    real_t *P0, *P1;         // P0 = caller phi, P1 = workspace copy
+    const real_t *F;         // speed
+    real_t *dd;              // delta / F (uniform solvers)
     // speed palette (piecewise-constant F): 1-byte index per cell + exact coefficient table
     uint8_t *pidx;
-    double *ptab;            // [PAL_MAX] delta/F_k (uniform) or F_k (anisotropic)
+    real_t *ptab;            // [PAL_MAX] delta/F_k (uniform) or F_k (anisotropic)
     unsigned long long *phash;  // [PAL_SLOTS] F bit patterns (open addressing)
     uint32_t *pslot;         // [PAL_SLOTS] slot -> palette index
     uint32_t *pstate;        // [0] distinct count, [1] overflow, [2] palette in use
@@ -160,21 +191,25 @@ struct KP {
 // Local solvers (bit-exact restatements; no FMA contraction)
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ double dmin(double a, double b) { return a <= b ? a : b; }
-__device__ __forceinline__ double dmax(double a, double b) { return a >= b ? a : b; }
+__device__ __forceinline__ real_t dmin(real_t a, real_t b) { return a <= b ? a : b; }
+__device__ __forceinline__ real_t dmax(real_t a, real_t b) { return a >= b ? a : b; }
 
 // sqrt(max(x, 0)) for the roots: x <= 0 (or NaN) yields +0 without feeding the
 // IEEE slow path (sqrt of 0/negative/NaN); the reference's clamp
 // `x if x > 0 else 0` (E/local_solver.py) gives exactly +0 there too.  Where
 // the numpy form would propagate NaN (E/_kernels.py:56, NaN disc) the root is
 // never selected (take_two / isfinite guards), so the result is unchanged.
-__device__ __forceinline__ double sqrt_rn(double x)
+__device__ __forceinline__ real_t sqrt_rn(real_t x)
 {
-    double r;  // opaque to the optimizer, so the operand select below is not folded away
+    real_t r;  // opaque to the optimizer, so the operand select below is not folded away
+#if EIK_SINGLE
+    asm("sqrt.rn.f32 %0, %1;" : "=f"(r) : "f"(x));
+#else
     asm("sqrt.rn.f64 %0, %1;" : "=d"(r) : "d"(x));
+#endif
     return r;
 }
-__device__ __forceinline__ double sqrt_pos(double x) { return x > 0.0 ? sqrt_rn(x > 0.0 ? x : 1.0) : 0.0; }
+__device__ __forceinline__ real_t sqrt_pos(real_t x) { return x > R_ZERO ? sqrt_rn(x > R_ZERO ? x : R_ONE) : R_ZERO; }
 
 // x / 3.0 correctly rounded without the division sequence (Markstein): inv3 =
 // RN(1/3) has relative error 2^-54, so q = RN(x * inv3) is within 3/4 ulp of
@@ -182,45 +217,49 @@ __device__ __forceinline__ double sqrt_pos(double x) { return x > 0.0 ? sqrt_rn(
 // correctly rounded quotient; x/3 is never a rounding tie.  Tiny (subnormal
 // quotient), zero and non-finite dividends take the IEEE division.  Checked
 // bit-exact against x / 3.0 on 3.4e10 values (tools/cuda/check_div3.cu).
-__device__ __forceinline__ double div3_rn(double x)
+__device__ __forceinline__ real_t div3_rn(real_t x)
 {
+#if EIK_SINGLE
+    return x / R_THREE;
+#else
     if (!(x >= 0x1p-900) || !(x < INFINITY)) return x / 3.0;
-    const double inv3 = 0x1.5555555555555p-2;
-    const double q = __dmul_rn(x, inv3);
-    const double r = __fma_rn(-q, 3.0, x);
+    const real_t inv3 = 0x1.5555555555555p-2;
+    const real_t q = __dmul_rn(x, inv3);
+    const real_t r = __fma_rn(-q, 3.0, x);
     return __fma_rn(r, inv3, q);
+#endif
 }
 
 // E/_kernels.py:47-58 (_update_uniform_batch), d = delta / f
-__device__ __forceinline__ double upd2u(double a, double b, double d)
+__device__ __forceinline__ real_t upd2u(real_t a, real_t b, real_t d)
 {
-    const double lo = dmin(a, b);
-    const double hi = dmax(a, b);
-    const double one = lo + d;
-    const double diff = hi - lo;
+    const real_t lo = dmin(a, b);
+    const real_t hi = dmax(a, b);
+    const real_t one = lo + d;
+    const real_t diff = hi - lo;
     const bool take_two = diff <= kSqrt2 * d;
-    const double disc = 2.0 * d * d - diff * diff;
-    const double root = 0.5 * (a + b + sqrt_pos(disc));
-    const bool valid = take_two && (disc >= -DISC_CLAMP * (2.0 * d * d)) && (root >= hi);
+    const real_t disc = R_TWO * d * d - diff * diff;
+    const real_t root = R_HALF * (a + b + sqrt_pos(disc));
+    const bool valid = take_two && (disc >= -DISC_CLAMP * (R_TWO * d * d)) && (root >= hi);
     return valid ? root : one;
 }
 
 // E/_kernels.py:61-88 (_update_aniso_batch)
-__device__ __forceinline__ double upd2a(double a, double b, double f, double dx, double dy)
+__device__ __forceinline__ real_t upd2a(real_t a, real_t b, real_t f, real_t dx, real_t dy)
 {
-    const double one_x = a + dx / f;
-    const double one_y = b + dy / f;
-    const double dx2 = dx * dx;
-    const double dy2 = dy * dy;
-    const double s2 = (dx2 + dy2) / (f * f);
-    const double s = sqrt(s2);
-    const double diff = a - b;
-    const double disc = s2 - diff * diff;
-    const double root = (a * dy2 + b * dx2 + (dx * dy) * sqrt_pos(disc)) / (dx2 + dy2);
-    const double drop_larger = (a > b) ? one_y : one_x;
+    const real_t one_x = a + dx / f;
+    const real_t one_y = b + dy / f;
+    const real_t dx2 = dx * dx;
+    const real_t dy2 = dy * dy;
+    const real_t s2 = (dx2 + dy2) / (f * f);
+    const real_t s = sqrt(s2);
+    const real_t diff = a - b;
+    const real_t disc = s2 - diff * diff;
+    const real_t root = (a * dy2 + b * dx2 + (dx * dy) * sqrt_pos(disc)) / (dx2 + dy2);
+    const real_t drop_larger = (a > b) ? one_y : one_x;
     const bool valid = isfinite(a) && isfinite(b) && !(diff > s) && !(-diff > s) &&
                        (disc >= -DISC_CLAMP * s2) && (root >= a) && (root >= b);
-    double out = valid ? root : drop_larger;
+    real_t out = valid ? root : drop_larger;
     if (isinf(a) && isfinite(b)) out = one_y;
     if (isfinite(a) && isinf(b)) out = one_x;
     if (isinf(a) && isinf(b)) out = INFINITY;
@@ -242,33 +281,33 @@ __device__ __forceinline__ double upd2a(double a, double b, double f, double dx,
 // ignores L2 because 1 was visited).  The selected value is produced by the
 // reference's own expression: bit-identical.  When every lane of the warp
 // takes the common "k0 = 3 and r3 valid" exit, branch 2 is not evaluated.
-__device__ __forceinline__ double upd3u(double px, double py, double pz, double d, double delta)
+__device__ __forceinline__ real_t upd3u(real_t px, real_t py, real_t pz, real_t d, real_t delta)
 {
-    double a1 = px, a2 = py, a3 = pz, t;
+    real_t a1 = px, a2 = py, a3 = pz, t;
     if (a2 < a1) { t = a1; a1 = a2; a2 = t; }
     if (a3 < a2) { t = a2; a2 = a3; a3 = t; }
     if (a2 < a1) { t = a1; a1 = a2; a2 = t; }
     const int k0 = (a3 - a1 < delta) ? 3 : ((a2 - a1 < delta) ? 2 : 1);
     // branch 3 (E/local_solver.py:119-134)
-    const double b2 = a2 - a1;
-    const double b3 = a3 - a1;
-    const double s3 = b2 + b3;
-    const double disc3 = s3 * s3 - 3.0 * (b2 * b2 + b3 * b3 - d * d);
-    const bool F3 = disc3 < -DISC_CLAMP * (3.0 * d * d);
+    const real_t b2 = a2 - a1;
+    const real_t b3 = a3 - a1;
+    const real_t s3 = b2 + b3;
+    const real_t disc3 = s3 * s3 - R_THREE * (b2 * b2 + b3 * b3 - d * d);
+    const bool F3 = disc3 < -DISC_CLAMP * (R_THREE * d * d);
     // r3 is only ever selected with a3 finite; an infinite dividend would take
     // the division slow path for a value nobody reads
-    const double x3 = s3 + sqrt_pos(disc3);
-    const double r3 = a1 + div3_rn(x3 < INFINITY ? x3 : 0.0);
+    const real_t x3 = s3 + sqrt_pos(disc3);
+    const real_t r3 = a1 + div3_rn(x3 < INFINITY ? x3 : R_ZERO);
     const bool quick = (a1 == INFINITY) || (k0 == 3 && !F3 && r3 >= a3);
     if (__all_sync(__activemask(), quick)) return a1 == INFINITY ? INFINITY : r3;
     // branch 2 (E/local_solver.py:136-151) and branch 1 (:152-157)
-    const double disc2 = 2.0 * d * d - b2 * b2;
-    const bool F2 = (a2 == INFINITY) || (disc2 < -DISC_CLAMP * (2.0 * d * d));
-    const double r2 = 0.5 * (a1 + a2 + sqrt_pos(disc2));
-    const double r1 = a1 + d;
+    const real_t disc2 = R_TWO * d * d - b2 * b2;
+    const bool F2 = (a2 == INFINITY) || (disc2 < -DISC_CLAMP * (R_TWO * d * d));
+    const real_t r2 = R_HALF * (a1 + a2 + sqrt_pos(disc2));
+    const real_t r1 = a1 + d;
     const bool L2 = r2 < a2, H2 = r2 > a3, H1 = r1 > a2;
-    const double M2 = H2 ? (F3 ? r2 : r3) : r2;
-    double out;
+    const real_t M2 = H2 ? (F3 ? r2 : r3) : r2;
+    real_t out;
     if (k0 == 3) out = (!F3 && r3 >= a3) ? r3 : ((F2 || L2) ? r1 : r2);
     else if (k0 == 2) out = (F2 || L2) ? r1 : M2;
     else out = (!H1 || F2) ? r1 : M2;
@@ -279,7 +318,22 @@ __device__ __forceinline__ double upd3u(double px, double py, double pz, double 
 // small helpers
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
+// Tolerance of the converge / build / decrease tests at value x.  float64: the
+// caller's absolute tol (E/ifim.py:121,157,203).  float32 perf mode: at least
+// 4 ulps of x, since a float32 Jacobi pair can otherwise alternate between
+// neighbouring floats forever (|v - old| = 1 ulp > 1e-12).
+__device__ __forceinline__ real_t tol_at(real_t tol, real_t x)
+{
+#if EIK_SINGLE
+    const real_t r = x * (real_t)0x1p-21;
+    return (r > tol && r < INFINITY) ? r : tol;  // an infinite old value keeps the absolute tol
+#else
+    (void)x;
+    return tol;
+#endif
+}
+
+__device__ __forceinline__ real_t ldcg(const real_t *p) { return __ldcg(p); }
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 template <typename T>
@@ -386,7 +440,7 @@ constexpr unsigned long long PAL_EMPTY = ~0ull;
 // (anisotropic), from the palette when the speed field has <= 255 distinct
 // values (same IEEE value, 1 byte of traffic instead of 8), else from the array.
 template <int SOL>
-__device__ __forceinline__ double coef(const KP &p, bool pal, uint32_t c)
+__device__ __forceinline__ real_t coef(const KP &p, bool pal, uint32_t c)
 {
     if (pal) return __ldg(p.ptab + __ldg(p.pidx + c));
     return (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
@@ -446,15 +500,15 @@ __device__ __forceinline__ WPos wpos(const KP &p, uint32_t w)
 // are +inf) plus the cell's coefficient (d = delta/F, or F for the
 // anisotropic solver).
 struct Sten {
-    double c, w, e, s, n, d, u, k;
-    double edge;  // word layout: lane 0 / lane 31 x-neighbour outside the word
+    real_t c, w, e, s, n, d, u, k;
+    real_t edge;  // word layout: lane 0 / lane 31 x-neighbour outside the word
 };
 
 // Word layout, stage 1: issue every load of the word at once (one memory
 // round trip).  Lanes adjacent to an active lane load their own value so the
 // x-neighbours come from shuffles in stage 2.
 template <int DIM, int SOL>
-__device__ __forceinline__ void gather_issue(const KP &p, const double *__restrict__ Pc, const WPos &q, uint32_t bits,
+__device__ __forceinline__ void gather_issue(const KP &p, const real_t *__restrict__ Pc, const WPos &q, uint32_t bits,
                                              Sten &s)
 {
     const unsigned lane = lane_id();
@@ -485,8 +539,8 @@ __device__ __forceinline__ void gather_issue(const KP &p, const double *__restri
 __device__ __forceinline__ void gather_finish(const KP &p, const WPos &q, Sten &s)
 {
     const unsigned lane = lane_id();
-    double w = __shfl_up_sync(FULL, s.c, 1);
-    double e = __shfl_down_sync(FULL, s.c, 1);
+    real_t w = __shfl_up_sync(FULL, s.c, 1);
+    real_t e = __shfl_down_sync(FULL, s.c, 1);
     if (lane == 0) w = s.edge;
     if (lane == 31) e = s.edge;
     else if (q.x0 + lane + 1 >= p.nx32) e = INFINITY;
@@ -495,7 +549,7 @@ __device__ __forceinline__ void gather_finish(const KP &p, const WPos &q, Sten &
 }
 
 template <int DIM, int SOL>
-__device__ __forceinline__ void gather(const KP &p, const double *__restrict__ Pc, const WPos &q, uint32_t bits,
+__device__ __forceinline__ void gather(const KP &p, const real_t *__restrict__ Pc, const WPos &q, uint32_t bits,
                                        Sten &s)
 {
     gather_issue<DIM, SOL>(p, Pc, q, bits, s);
@@ -504,10 +558,10 @@ __device__ __forceinline__ void gather(const KP &p, const double *__restrict__ P
 
 // One local-solver call on the gathered stencil (E/ifim.py:57-59).
 template <int DIM, int SOL>
-__device__ __forceinline__ double solve(const KP &p, const Sten &s)
+__device__ __forceinline__ real_t solve(const KP &p, const Sten &s)
 {
-    const double xm = dmin(s.w, s.e);
-    const double ym = dmin(s.s, s.n);
+    const real_t xm = dmin(s.w, s.e);
+    const real_t ym = dmin(s.s, s.n);
     if (SOL == SOL_U2) return upd2u(xm, ym, s.k);
     if (SOL == SOL_A2) return upd2a(xm, ym, s.k, p.dx, p.dy);
     return upd3u(xm, ym, dmin(s.d, s.u), s.k, p.delta);
@@ -556,7 +610,7 @@ __device__ __forceinline__ unsigned block_reserve(unsigned v, unsigned *glen, un
 __device__ __forceinline__ bool ghost_plane(const KP &p, uint32_t z) { return p.slab && (z == 0 || z + 1 == (uint32_t)p.nz); }
 
 // apply_boundary writes (E/grid.py:212-215); validation is done by the caller.
-__global__ void k_seed(double *phi, uint8_t *state, const int64_t *idx, const double *val, int64_t n)
+__global__ void k_seed(real_t *phi, uint8_t *state, const int64_t *idx, const double *val, int64_t n)
 {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
         phi[idx[s]] = val[s];
@@ -581,7 +635,7 @@ __global__ void k_palette_insert(KP p, int64_t n)
         if (*(volatile uint32_t *)(p.pstate + 1)) return;  // overflow: give up
         const int64_t i = i0 + lane;
         const bool in = i < n;
-        const unsigned long long key = in ? (unsigned long long)__double_as_longlong(p.F[i]) : PAL_EMPTY;
+        const unsigned long long key = in ? bits_of(p.F[i]) : PAL_EMPTY;
         const unsigned grp = __match_any_sync(FULL, key);
         if (!in || lane != (unsigned)(__ffs(grp) - 1)) continue;
         uint32_t h = pal_hash(key);
@@ -615,16 +669,16 @@ __global__ void k_palette_finalize(KP p)
         if (!ok || key == PAL_EMPTY) continue;
         const uint32_t k = atomicAdd(&cnt, 1u);
         p.pslot[s] = k;
-        const double f = __longlong_as_double((long long)key);
+        const real_t f = real_of_bits(key);
         p.ptab[k] = UNIFORM ? p.delta / f : f;
     }
     __syncthreads();
     if (threadIdx.x == 0) p.pstate[2] = ok ? 1u : 0u;
 }
 
-__device__ __forceinline__ uint8_t pal_index(const KP &p, double f)
+__device__ __forceinline__ uint8_t pal_index(const KP &p, real_t f)
 {
-    const unsigned long long key = (unsigned long long)__double_as_longlong(f);
+    const unsigned long long key = bits_of(f);
     uint32_t h = pal_hash(key);
     while (__ldg(p.phash + h) != key) h = (h + 1) & (PAL_SLOTS - 1);
     return (uint8_t)__ldg(p.pslot + h);
@@ -661,7 +715,8 @@ __global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_
 }
 
 // Multi-rank: write the seeds this rank owns (global linear index -> local).
-__global__ void k_seed_mr(double *phi, uint8_t *state, const int64_t *idx, const double *val, int64_t n, int64_t zg0,
+#if !EIK_SINGLE
+__global__ void k_seed_mr(real_t *phi, uint8_t *state, const int64_t *idx, const double *val, int64_t n, int64_t zg0,
                           int64_t nzl, int64_t plane)
 {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < n; s += (int64_t)gridDim.x * blockDim.x) {
@@ -672,9 +727,11 @@ __global__ void k_seed_mr(double *phi, uint8_t *state, const int64_t *idx, const
         state[c] = ST_SOURCE;
     }
 }
+#endif
 
 // Multi-rank initial activation: every seed (global index) activates the free
 // FAR neighbours this rank owns (E/ifim.py:97-102).
+#if !EIK_SINGLE
 __global__ void k_init_active_mr(KP p, const int64_t *seeds, int64_t nseeds, int64_t zg0, int64_t nz_global)
 {
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nseeds; s += (int64_t)gridDim.x * blockDim.x) {
@@ -695,6 +752,7 @@ __global__ void k_init_active_mr(KP p, const int64_t *seeds, int64_t nseeds, int
         }
     }
 }
+#endif
 
 // Initial Active = free FAR axis neighbours of the seeds (E/ifim.py:97-102).
 template <int DIM>
@@ -787,8 +845,8 @@ __device__ __forceinline__ void update_body(const KP &p)
     const bool pal = palette_on(p);
     for (int64_t it = p.it0; it < p.it0 + p.max_it; ++it) {
         const int par = (int)(it & 1);
-        const double *__restrict__ Pc = par ? p.P1 : p.P0;
-        double *__restrict__ Pn = par ? p.P0 : p.P1;
+        const real_t *__restrict__ Pc = par ? p.P1 : p.P0;
+        real_t *__restrict__ Pn = par ? p.P0 : p.P1;
         const uint32_t *__restrict__ Lc = par ? p.L1 : p.L0;
         uint32_t *Ln = par ? p.L0 : p.L1;
         unsigned *lenN = &ctl->len[(it + 1) % 3];
@@ -841,9 +899,9 @@ __device__ __forceinline__ void update_body(const KP &p)
             for (int u = 0; u < UPD_MU; ++u) {
                 if (!live[u]) continue;
                 const Sten &t = s[u];
-                const double v = solve<DIM, SOL>(p, t);
+                const real_t v = solve<DIM, SOL>(p, t);
                 // E/ifim.py:121: converged iff v == old or |v - old| <= tol
-                const bool conv = (v == t.c) || fabs(v - t.c) <= p.tol;
+                const bool conv = (v == t.c) || fabs(v - t.c) <= tol_at(p.tol, t.c);
                 if (!conv) Pn[c[u]] = v;              // E/ifim.py:128
                 else if (carry[u]) Pn[c[u]] = t.c;    // changed last iteration: carry into the other buffer
                 if (!conv) {
@@ -852,7 +910,7 @@ __device__ __forceinline__ void update_body(const KP &p)
                 } else {
                     ++a_conv;
                     // activate +inf, unblocked, FAR neighbours (E/ifim.py:123-126)
-                    const double nv[6] = {t.w, t.e, t.s, t.n, t.d, t.u};
+                    const real_t nv[6] = {t.w, t.e, t.s, t.n, t.d, t.u};
                     uint32_t old[6];
 #pragma unroll
                     for (int k = 0; k < (DIM == 3 ? 6 : 4); ++k) {
@@ -953,7 +1011,7 @@ __global__ void __launch_bounds__(BLOCK, 3) k_update_mr(const KP *__restrict__ k
 // ---------------------------------------------------------------------------
 
 template <int DIM, int SOL>
-__global__ void __launch_bounds__(BLOCK) k_build(KP p, const double *__restrict__ Pc, const unsigned *skip)
+__global__ void __launch_bounds__(BLOCK) k_build(KP p, const real_t *__restrict__ Pc, const unsigned *skip)
 {
     __shared__ unsigned long long sred[WPB];
     if (skip && *skip) return;
@@ -971,8 +1029,8 @@ __global__ void __launch_bounds__(BLOCK) k_build(KP p, const double *__restrict_
             gather<DIM, SOL>(p, Pc, q, freem, s);
             bool moved = false;
             if ((freem >> lane) & 1u) {
-                const double v = solve<DIM, SOL>(p, s);
-                moved = fabs(v - s.c) > p.tol;  // NaN (inf - inf) is not flagged
+                const real_t v = solve<DIM, SOL>(p, s);
+                moved = fabs(v - s.c) > tol_at(p.tol, s.c);  // NaN (inf - inf) is not flagged
             }
             mm = __ballot_sync(FULL, moved);
         }
@@ -1166,8 +1224,8 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
         if (lead) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dgt0));
 #endif
         const int par = (int)(r & 1);
-        const double *__restrict__ Pc = par ? p.P1 : p.P0;
-        double *__restrict__ Pn = par ? p.P0 : p.P1;
+        const real_t *__restrict__ Pc = par ? p.P1 : p.P0;
+        real_t *__restrict__ Pn = par ? p.P0 : p.P1;
         uint32_t *Dc = par ? p.D1b : p.D0b;
         const uint32_t *Dp = par ? p.D0b : p.D1b;
         unsigned *lenR = &ctl->len[r % 3];
@@ -1226,7 +1284,7 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
 #if REM_PREF > 1
                 if (j < mend) {  // warm L2 with the next member's rows (no registers held)
                     const uint32_t cn = nent[u] & ~CARRY;
-                    const double *b = Pc + cn;
+                    const real_t *b = Pc + cn;
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(b));
                     asm volatile("prefetch.global.L2 [%0];" ::"l"(p.dd + cn));
                     if (cn >= nx) asm volatile("prefetch.global.L2 [%0];" ::"l"(b - nx));
@@ -1278,8 +1336,8 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
                 const uint32_t c = ent[u] & ~CARRY;
                 bool dec = false;
                 if (live[u]) {
-                    const double v = solve<DIM, SOL>(p, s[u]);
-                    dec = v < s[u].c - p.tol;  // E/ifim.py:203
+                    const real_t v = solve<DIM, SOL>(p, s[u]);
+                    dec = v < s[u].c - tol_at(p.tol, s[u].c);  // E/ifim.py:203
                     if (dec) Pn[c] = v;
                     else if (ent[u] & CARRY) Pn[c] = s[u].c;  // changed last round: carry into the other buffer
                 }
@@ -1355,8 +1413,8 @@ __global__ void __launch_bounds__(BLOCK) k_fixpoint(KP p)
     const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
     for (int64_t it = 0;; ++it) {
         const int par = (int)(it & 1);
-        const double *__restrict__ Pc = par ? p.P1 : p.P0;
-        double *__restrict__ Pn = par ? p.P0 : p.P1;
+        const real_t *__restrict__ Pc = par ? p.P1 : p.P0;
+        real_t *__restrict__ Pn = par ? p.P0 : p.P1;
         unsigned long long a_dec = 0, a_max = 0;
         for (uint32_t w = gw; w < p.nwords; w += GW) {
             const WPos q = wpos<DIM>(p, w);
@@ -1366,12 +1424,12 @@ __global__ void __launch_bounds__(BLOCK) k_fixpoint(KP p)
             gather<DIM, SOL>(p, Pc, q, freem, s);
             bool dec = false;
             if ((freem >> lane) & 1u) {
-                const double cand = solve<DIM, SOL>(p, s);
-                const double nw = dmin(s.c, cand);  // np.minimum(old, candidates)
+                const real_t cand = solve<DIM, SOL>(p, s);
+                const real_t nw = dmin(s.c, cand);  // np.minimum(old, candidates)
                 dec = nw < s.c;
                 if (dec) {
-                    const double ch = s.c - nw;
-                    const unsigned long long b = (unsigned long long)__double_as_longlong(ch);
+                    const real_t ch = s.c - nw;
+                    const unsigned long long b = bits_of(ch);
                     if (b > a_max) a_max = b;
                 }
                 Pn[q.c0 + lane] = nw;
@@ -1396,7 +1454,7 @@ __global__ void __launch_bounds__(BLOCK) k_fixpoint(KP p)
         }
         if (!grid_barrier(ctl)) return;
         const unsigned long long decs = vload(&ctl->dsum[it % 3]);
-        const double maxch = __longlong_as_double((long long)vload(&ctl->cnt[it % 3]));
+        const real_t maxch = real_of_bits(vload(&ctl->cnt[it % 3]));
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->iters = it + 1;
         if (decs == 0 || maxch < p.tol) break;  // E/oracle.py:59-62
         if (it + 1 >= p.cap) {                   // E/oracle.py:63-67
@@ -1422,8 +1480,8 @@ __global__ void __launch_bounds__(BLOCK) k_residual(KP p)
         Sten s;
         gather<DIM, SOL>(p, p.P0, q, freem, s);
         if (((freem >> lane) & 1u) && s.c < INFINITY) {
-            const double r = fabs(s.c - solve<DIM, SOL>(p, s));
-            const unsigned long long b = (unsigned long long)__double_as_longlong(r);
+            const real_t r = fabs(s.c - solve<DIM, SOL>(p, s));
+            const unsigned long long b = bits_of(r);
             if (r == r && b > a_max) a_max = b;
         }
     }
@@ -1439,6 +1497,7 @@ __global__ void __launch_bounds__(BLOCK) k_residual(KP p)
 // touched words) for the owned boundary planes; a requested cell is activated
 // iff it is still FAR here (blocked cells are pre-touched).  The requester's
 // +inf test used the same snapshot value.  Appends to the next list of `it`.
+#if !EIK_SINGLE
 __global__ void k_apply_requests(KP p, const uint32_t *req_lo, const uint32_t *req_hi, int64_t it)
 {
     const uint32_t planeW = (uint32_t)p.ny * p.W;
@@ -1459,10 +1518,11 @@ __global__ void k_apply_requests(KP p, const uint32_t *req_lo, const uint32_t *r
         for (uint32_t b = nb; b; b &= b - 1) Ln[atomicAdd(lenN, 1u)] = c0 + (uint32_t)(__ffs(b) - 1);
     }
 }
+#endif
 
 // Element-wise local solver (parity hook).
-__global__ void k_local(int kind, const double *a, const double *b, const double *c, const double *f, double dx,
-                        double dy, double *out, int64_t n)
+__global__ void k_local(int kind, const real_t *a, const real_t *b, const real_t *c, const real_t *f, real_t dx,
+                        real_t dy, real_t *out, int64_t n)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         if (kind == 0) out[i] = upd2u(a[i], b[i], dx / f[i]);
@@ -1514,7 +1574,8 @@ int make_layout(const eik_geom *g, Layout &L)
     if (!(g->dx > 0) || !(g->dy > 0) || !(g->dz > 0)) return fail(EIK_EINVAL, "grid spacing must be positive");
     if (g->ndim == 3 && !(g->dx == g->dy && g->dy == g->dz))
         return fail(EIK_EINVAL, "3D grids require dx == dy == dz (no anisotropic 3D solver, SPEC.md:169)");
-    if (g->dtype != EIK_F64) return fail(EIK_EINVAL, "only float64 is supported");
+    if (g->dtype != EIK_DTYPE)
+        return fail(EIK_EINVAL, EIK_SINGLE ? "this library is the float32 engine (dtype EIK_SINGLE)" : "this library is the float64 engine (dtype EIK_F64)");
     if ((g->flags & EIK_GEOM_SLAB) && (g->ndim != 3 || g->nz < 3))
         return fail(EIK_EINVAL, "a slab is 3D with at least one owned plane plus two ghost planes");
     L.N = g->nx * g->ny * g->nz;
@@ -1529,8 +1590,8 @@ int make_layout(const eik_geom *g, Layout &L)
     L.cap_rem = 20 * s;  // E/ifim.py:185
     const size_t bm = (size_t)nw * 4;
     size_t o = 0;
-    L.off_phi2 = o; o += al((size_t)L.N * 8);
-    L.off_dd = o; o += al((size_t)L.N * 8);
+    L.off_phi2 = o; o += al((size_t)L.N * sizeof(real_t));
+    L.off_dd = o; o += al((size_t)L.N * sizeof(real_t));
     L.off_bt = o; o += al(bm);
     L.off_l0 = o; o += al((size_t)L.N * 4);  // update: active cells; remedy: members
     L.off_l1 = o; o += al((size_t)L.N * 4);
@@ -1539,7 +1600,7 @@ int make_layout(const eik_geom *g, Layout &L)
     L.off_d1 = o; o += al(bm);
     L.off_f = o; o += al(bm);
     L.off_pidx = o; o += al((size_t)L.N);
-    L.off_ptab = o; o += al(PAL_MAX * 8 + 8);
+    L.off_ptab = o; o += al(PAL_MAX * sizeof(real_t) + 8);
     L.off_phash = o; o += al(PAL_SLOTS * 8);
     L.off_pslot = o; o += al(PAL_SLOTS * 4);
     L.off_pstate = o; o += al(16);
@@ -1567,7 +1628,7 @@ int solver_kind(const eik_geom *g)
     return g->dx == g->dy ? SOL_U2 : SOL_A2;  // E/_kernels.py:41-44
 }
 
-KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const double *speed, const uint8_t *state,
+KP make_kp(const eik_geom *g, const Layout &L, void *ws, real_t *phi, const real_t *speed, const uint8_t *state,
            double tol, Ctl *ctl, int64_t cap)
 {
     char *b = (char *)ws;
@@ -1589,9 +1650,9 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const doub
     p.it0 = 0;
     p.max_it = (int64_t)1 << 40;
     p.P0 = phi;
-    p.P1 = (double *)(b + L.off_phi2);
+    p.P1 = (real_t *)(b + L.off_phi2);
     p.F = speed;
-    p.dd = (double *)(b + L.off_dd);
+    p.dd = (real_t *)(b + L.off_dd);
     p.state = state;
     p.Bt = (uint32_t *)(b + L.off_bt);
     p.L0 = (uint32_t *)(b + L.off_l0);
@@ -1605,7 +1666,7 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, double *phi, const doub
     p.D1b = (uint32_t *)(b + L.off_d1);
     p.Fb = (uint32_t *)(b + L.off_f);
     p.pidx = (uint8_t *)(b + L.off_pidx);
-    p.ptab = (double *)(b + L.off_ptab);
+    p.ptab = (real_t *)(b + L.off_ptab);
     p.phash = (unsigned long long *)(b + L.off_phash);
     p.pslot = (uint32_t *)(b + L.off_pslot);
     p.pstate = (uint32_t *)(b + L.off_pstate);
@@ -1717,7 +1778,7 @@ struct Engine {
         }
         return EIK_OK;
     }
-    static int build(KP &p, const double *Pc, const unsigned *skip, cudaStream_t st)
+    static int build(KP &p, const real_t *Pc, const unsigned *skip, cudaStream_t st)
     {
         int rc = reset_set(p, st);
         if (rc) return rc;
@@ -1794,7 +1855,7 @@ int check_ws(const Layout &L, void *ws, size_t bytes)
     return EIK_OK;
 }
 
-int run_update(const eik_geom *g, const Layout &L, double *phi, const double *speed, uint8_t *state,
+int run_update(const eik_geom *g, const Layout &L, real_t *phi, const real_t *speed, uint8_t *state,
                const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol, void *ws,
                cudaStream_t st, int64_t &launches)
 {
@@ -1836,7 +1897,7 @@ void fill_update_stats(const Ctl &c, eik_stats *o)
     o->history_len = (int64_t)c.iters;
 }
 
-int expose_latest(const Layout &L, const Ctl &c, double *phi, const double *phi2, cudaStream_t st)
+int expose_latest(const Layout &L, const Ctl &c, real_t *phi, const real_t *phi2, cudaStream_t st)
 {
     if (c.iters & 1) {  // the newest values sit in the workspace buffer
         CK(cudaMemcpyAsync(phi, phi2, (size_t)L.N * 8, cudaMemcpyDeviceToDevice, st));
@@ -1853,14 +1914,18 @@ int expose_latest(const Layout &L, const Ctl &c, double *phi, const double *phi2
 
 extern "C" {
 
-const char *eik_last_error(void) { return g_err.c_str(); }
+const char *EIK_FN(eik_last_error)(void) { return g_err.c_str(); }
 
-const char *eik_version(void)
+const char *EIK_FN(eik_version)(void)
 {
-    return "eik_ifim 0.3 (sm_100a, float64 bit-exact; persistent cell-worklist update + member-list remedy)";
+#if EIK_SINGLE
+    return "eik_ifim 0.4 (sm_100a, float32 perf mode; persistent cell-worklist update + member-list remedy)";
+#else
+    return "eik_ifim 0.4 (sm_100a, float64 bit-exact; persistent cell-worklist update + member-list remedy)";
+#endif
 }
 
-int eik_workspace_size(const eik_geom *g, size_t *bytes)
+int EIK_FN(eik_workspace_size)(const eik_geom *g, size_t *bytes)
 {
     Layout L;
     int rc = make_layout(g, L);
@@ -1870,7 +1935,7 @@ int eik_workspace_size(const eik_geom *g, size_t *bytes)
     return EIK_OK;
 }
 
-int eik_ifim_update_step(const eik_geom *g, double *phi, const double *speed, uint8_t *state,
+int EIK_FN(eik_ifim_update_step)(const eik_geom *g, real_t *phi, const real_t *speed, uint8_t *state,
                          const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
                          void *workspace, size_t workspace_bytes, int64_t *history, int64_t history_cap,
                          eik_stats *out, void *stream)
@@ -1906,13 +1971,13 @@ int eik_ifim_update_step(const eik_geom *g, double *phi, const double *speed, ui
         CK(cudaMemcpy(history, b + L.off_hist, (size_t)n * 8, cudaMemcpyDeviceToHost));
     }
     if (c.err == EIK_ECAP) {
-        if ((rc = expose_latest(L, c, phi, (const double *)(b + L.off_phi2), st))) return rc;
+        if ((rc = expose_latest(L, c, phi, (const real_t *)(b + L.off_phi2), st))) return rc;
         return fail(EIK_ECAP, "active list did not drain within %lld iterations", (long long)L.cap_upd);
     }
     return EIK_OK;
 }
 
-int eik_build_remedy(const eik_geom *g, const double *phi, const double *speed, const uint8_t *state, double tol,
+int EIK_FN(eik_build_remedy)(const eik_geom *g, const real_t *phi, const real_t *speed, const uint8_t *state, double tol,
                      void *workspace, size_t workspace_bytes, eik_stats *out, void *stream)
 {
     Layout L;
@@ -1927,7 +1992,7 @@ int eik_build_remedy(const eik_geom *g, const double *phi, const double *speed, 
     Ctl *ctl = (Ctl *)(b + L.off_ctl_r);
     Events ev;
     ev.rec(0, st);
-    KP p = make_kp(g, L, workspace, const_cast<double *>(phi), speed, state, tol, ctl, L.cap_rem);
+    KP p = make_kp(g, L, workspace, const_cast<real_t *>(phi), speed, state, tol, ctl, L.cap_rem);
     rc = dispatch(g, [&](auto E) {
         int r = E.prep(p, false, false, st);
         if (r) return r;
@@ -1945,7 +2010,7 @@ int eik_build_remedy(const eik_geom *g, const double *phi, const double *speed, 
     return EIK_OK;
 }
 
-int eik_remedy_load(const eik_geom *g, const uint8_t *member, const uint8_t *state, void *workspace,
+int EIK_FN(eik_remedy_load)(const eik_geom *g, const uint8_t *member, const uint8_t *state, void *workspace,
                     size_t workspace_bytes, int64_t *count, void *stream)
 {
     Layout L;
@@ -1966,7 +2031,7 @@ int eik_remedy_load(const eik_geom *g, const uint8_t *member, const uint8_t *sta
     return EIK_OK;
 }
 
-int eik_remedy_export(const eik_geom *g, void *workspace, size_t workspace_bytes, uint8_t *member, void *stream)
+int EIK_FN(eik_remedy_export)(const eik_geom *g, void *workspace, size_t workspace_bytes, uint8_t *member, void *stream)
 {
     Layout L;
     int rc = make_layout(g, L);
@@ -1986,7 +2051,7 @@ int eik_remedy_export(const eik_geom *g, void *workspace, size_t workspace_bytes
     return EIK_OK;
 }
 
-int eik_remedy_step(const eik_geom *g, double *phi, const double *speed, const uint8_t *state, double tol,
+int EIK_FN(eik_remedy_step)(const eik_geom *g, real_t *phi, const real_t *speed, const uint8_t *state, double tol,
                     void *workspace, size_t workspace_bytes, eik_stats *out, void *stream)
 {
     Layout L;
@@ -2027,7 +2092,7 @@ int eik_remedy_step(const eik_geom *g, double *phi, const double *speed, const u
     return EIK_OK;
 }
 
-int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t *state, const int64_t *seed_idx,
+int EIK_FN(eik_ifim_solve)(const eik_geom *g, real_t *phi, const real_t *speed, uint8_t *state, const int64_t *seed_idx,
                    const double *seed_val, int64_t nseeds, double tol, void *workspace, size_t workspace_bytes,
                    int64_t *history, int64_t history_cap, eik_stats *out, void *stream)
 {
@@ -2107,7 +2172,7 @@ int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t 
     return EIK_OK;
 }
 
-int eik_solve_fixpoint(const eik_geom *g, double *phi, const double *speed, uint8_t *state,
+int EIK_FN(eik_solve_fixpoint)(const eik_geom *g, real_t *phi, const real_t *speed, uint8_t *state,
                        const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
                        int64_t max_passes, void *workspace, size_t workspace_bytes, eik_stats *out, void *stream)
 {
@@ -2162,7 +2227,7 @@ int eik_solve_fixpoint(const eik_geom *g, double *phi, const double *speed, uint
     return EIK_OK;
 }
 
-int eik_max_residual(const eik_geom *g, const double *phi, const double *speed, const uint8_t *state,
+int EIK_FN(eik_max_residual)(const eik_geom *g, const real_t *phi, const real_t *speed, const uint8_t *state,
                      void *workspace, size_t workspace_bytes, double *out, void *stream)
 {
     Layout L;
@@ -2173,7 +2238,7 @@ int eik_max_residual(const eik_geom *g, const double *phi, const double *speed, 
     cudaStream_t st = (cudaStream_t)stream;
     Ctl *ctl = (Ctl *)((char *)workspace + L.off_ctl_r);
     CK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
-    KP p = make_kp(g, L, workspace, const_cast<double *>(phi), speed, state, 1e-12, ctl, 0);
+    KP p = make_kp(g, L, workspace, const_cast<real_t *>(phi), speed, state, 1e-12, ctl, 0);
     rc = dispatch(g, [&](auto E) {
         int r = E.prep(p, false, false, st);
         if (r) return r;
@@ -2184,12 +2249,19 @@ int eik_max_residual(const eik_geom *g, const double *phi, const double *speed, 
     CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     unsigned long long bits = c.peak;
+#if EIK_SINGLE
+    const unsigned b32 = (unsigned)bits;
+    float r;
+    memcpy(&r, &b32, 4);
+#else
     double r;
     memcpy(&r, &bits, 8);
-    *out = r;  // 0.0 when no free finite cell (E/harness.py:158-159)
+#endif
+    *out = (double)r;  // 0.0 when no free finite cell (E/harness.py:158-159)
     return EIK_OK;
 }
 
+#if !EIK_SINGLE  // multi-GPU slabs: float64 engine only
 // ---- multi-rank (peer slabs) -----------------------------------------------
 
 static Peer make_peer(const eik_geom *g, const eik_rank &rk, int use_remedy)
@@ -2203,7 +2275,7 @@ static Peer make_peer(const eik_geom *g, const eik_rank &rk, int use_remedy)
     if (make_layout(&gl, L)) return pr;
     char *b = (char *)rk.workspace;
     pr.P0 = rk.phi0;
-    pr.P1 = (double *)(b + L.off_phi2);
+    pr.P1 = (real_t *)(b + L.off_phi2);
     pr.Bt = (uint32_t *)(b + L.off_bt);
     pr.L0 = (uint32_t *)(b + L.off_l0);
     pr.L1 = (uint32_t *)(b + L.off_l1);
@@ -2221,7 +2293,7 @@ struct MrCtx {
     KP kp;
 };
 
-static int mr_setup(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t q, const double *speed,
+static int mr_setup(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t q, const real_t *speed,
                     uint8_t *state, double tol, int use_remedy, MrCtx &m)
 {
     if (!g || g->ndim != 3 || g->flags) return fail(EIK_EINVAL, "multi-rank solves take the global 3D geometry");
@@ -2273,7 +2345,7 @@ int eik_peer_enable(int32_t device, int32_t peer)
 }
 
 int eik_mr_prepare(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_begin, int32_t r_end,
-                   const double *const *speed, uint8_t *const *state, const int64_t *seeds, const double *seed_val,
+                   const real_t *const *speed, uint8_t *const *state, const int64_t *seeds, const double *seed_val,
                    int64_t nseeds, double tol, void *stream)
 {
     if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
@@ -2304,7 +2376,7 @@ int eik_mr_prepare(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t 
 }
 
 int eik_mr_run(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_begin, int32_t r_end,
-               const double *const *speed, uint8_t *const *state, double tol, int64_t *history, int64_t history_cap,
+               const real_t *const *speed, uint8_t *const *state, double tol, int64_t *history, int64_t history_cap,
                eik_stats *out, void *stream)
 {
     if (r_begin < 0 || r_end > R || r_begin >= r_end) return fail(EIK_EINVAL, "bad local rank range");
@@ -2425,7 +2497,7 @@ static int slab_check(const eik_geom *g, Layout &L, void *ws, size_t wsb)
     return check_ws(L, ws, wsb);
 }
 
-int eik_slab_update_init(const eik_geom *g, double *phi, const double *speed, uint8_t *state, const int64_t *seed_idx,
+int eik_slab_update_init(const eik_geom *g, real_t *phi, const real_t *speed, uint8_t *state, const int64_t *seed_idx,
                          const double *seed_val, int64_t nseeds, double tol, void *workspace, size_t workspace_bytes,
                          int64_t *n_active, void *stream)
 {
@@ -2459,7 +2531,7 @@ int eik_slab_update_init(const eik_geom *g, double *phi, const double *speed, ui
     return EIK_OK;
 }
 
-int eik_slab_update_iter(const eik_geom *g, double *phi, const double *speed, uint8_t *state, double tol, int64_t it,
+int eik_slab_update_iter(const eik_geom *g, real_t *phi, const real_t *speed, uint8_t *state, double tol, int64_t it,
                          void *workspace, size_t workspace_bytes, void *stream)
 {
     Layout L;
@@ -2495,7 +2567,7 @@ int eik_slab_apply_requests(const eik_geom *g, const uint32_t *req_lo, const uin
     return EIK_OK;
 }
 
-int eik_slab_build(const eik_geom *g, const double *phi, const double *speed, const uint8_t *state, double tol,
+int eik_slab_build(const eik_geom *g, const real_t *phi, const real_t *speed, const uint8_t *state, double tol,
                    void *workspace, size_t workspace_bytes, int64_t *free_cells, int64_t *flagged, void *stream)
 {
     Layout L;
@@ -2504,7 +2576,7 @@ int eik_slab_build(const eik_geom *g, const double *phi, const double *speed, co
     if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
     cudaStream_t st = (cudaStream_t)stream;
     Ctl *ctl = (Ctl *)((char *)workspace + L.off_ctl_r);
-    KP p = make_kp(g, L, workspace, const_cast<double *>(phi), speed, state, tol, ctl, L.cap_rem);
+    KP p = make_kp(g, L, workspace, const_cast<real_t *>(phi), speed, state, tol, ctl, L.cap_rem);
     rc = dispatch(g, [&](auto E) { return E.build(p, phi, nullptr, st); });
     if (rc) return rc;
     Ctl c;
@@ -2515,7 +2587,7 @@ int eik_slab_build(const eik_geom *g, const double *phi, const double *speed, co
     return EIK_OK;
 }
 
-int eik_slab_remedy_round(const eik_geom *g, double *phi, const double *speed, const uint8_t *state, double tol,
+int eik_slab_remedy_round(const eik_geom *g, real_t *phi, const real_t *speed, const uint8_t *state, double tol,
                           int64_t r, void *workspace, size_t workspace_bytes, int64_t *calls, int64_t *decs,
                           void *stream)
 {
@@ -2543,14 +2615,17 @@ int eik_slab_remedy_round(const eik_geom *g, double *phi, const double *speed, c
     return EIK_OK;
 }
 
-int eik_local_solve(int kind, const double *a, const double *b, const double *c, const double *f, double dx,
-                    double dy, double *out, int64_t n, void *stream)
+#endif  // !EIK_SINGLE
+
+int EIK_FN(eik_local_solve)(int kind, const real_t *a, const real_t *b, const real_t *c, const real_t *f, double dx,
+                    double dy, real_t *out, int64_t n, void *stream)
 {
     if (kind < 0 || kind > 2) return fail(EIK_EINVAL, "kind must be 0, 1 or 2");
     if (!a || !b || !f || !out || (kind == 2 && !c)) return fail(EIK_EINVAL, "null array");
     if (n <= 0) return EIK_OK;
     cudaStream_t st = (cudaStream_t)stream;
-    k_local<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(kind, a, b, c, f, dx, dy, out, n);
+    k_local<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(kind, a, b, c, f, (real_t)dx, (real_t)dy,
+                                                                          out, n);
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(st));
     return EIK_OK;

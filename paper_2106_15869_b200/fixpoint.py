@@ -37,14 +37,14 @@ def solve_fixpoint(grid, bc, tol: float = 1e-12, workers: int = 1, max_passes: i
     sv = torch.as_tensor(val, dtype=torch.float64, device=dg.device)
     st = _native.Stats()
     out = _HostResult(dg)
-    rc = _native.lib().eik_solve_fixpoint(C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), _ptr(si),
+    rc = _native.lib(geom.dtype).eik_solve_fixpoint(C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), _ptr(si),
                                           _ptr(sv), len(idx), float(tol), int(max_passes or 0), ws.ptr, ws.nbytes,
                                           C.byref(st), dg.stream)
     phi = None
     if dg.host:
         _host_mark_sources(grid, idx)
         phi = out.commit()
-    _native.check(rc)
+    _native.check(rc, geom.dtype)
     stats = RunStats(iterations=int(st.iterations), solver_calls=int(st.solver_calls))
     stats.device_ms = {"total": float(st.total_ms)}
     stats.gpu_launches = int(st.gpu_launches)
@@ -61,6 +61,6 @@ def max_residual(grid) -> float:
     ws = workspace(geom, dg.device)
     ws.gen += 1
     out = C.c_double(0.0)
-    _native.check(_native.lib().eik_max_residual(C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state),
+    _native.check(_native.lib(geom.dtype).eik_max_residual(C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state),
                                                  ws.ptr, ws.nbytes, C.byref(out), dg.stream))
     return float(out.value)

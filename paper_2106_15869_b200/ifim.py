@@ -63,11 +63,18 @@ def _pick_device(grid) -> torch.device:
     return torch.device(dev)
 
 
+def field_dtype(grid) -> int:
+    """float32 phi selects the float32 perf-mode engine; anything else runs in float64."""
+    d = getattr(grid.phi, "dtype", None)
+    return _native.EIK_F32 if d in (torch.float32, np.float32) else _native.EIK_F64
+
+
 def geometry(grid) -> _native.Geom:
+    dt = field_dtype(grid)
     if getattr(grid, "ndim", 2) == 3:
         h = float(grid.h)
-        return _native.Geom(int(grid.nx), int(grid.ny), int(grid.nz), h, h, h, 3, 0, 0, 0)
-    return _native.Geom(int(grid.nx), int(grid.ny), 1, float(grid.dx), float(grid.dy), float(grid.dx), 2, 0, 0, 0)
+        return _native.Geom(int(grid.nx), int(grid.ny), int(grid.nz), h, h, h, 3, dt, 0, 0)
+    return _native.Geom(int(grid.nx), int(grid.ny), 1, float(grid.dx), float(grid.dy), float(grid.dx), 2, dt, 0, 0)
 
 
 class _DeviceGrid:
@@ -82,8 +89,9 @@ class _DeviceGrid:
         self.grid = grid
         self.device = _pick_device(grid)
         self.host = not _is_cuda_tensor(grid.phi)
-        self.phi = self._dev(grid.phi, torch.float64) if need_phi else None
-        self.speed = self._dev(grid.speed, torch.float64)
+        self.dtype = torch.float32 if field_dtype(grid) == _native.EIK_F32 else torch.float64
+        self.phi = self._dev(grid.phi, self.dtype) if need_phi else None
+        self.speed = self._dev(grid.speed, self.dtype)
         self.state = self._dev(grid.state, torch.uint8) if need_state else None
 
     def _dev(self, arr, dtype):
@@ -143,9 +151,9 @@ class _HostResult:
 
             def alloc():
                 if self.pinned:
-                    self.buf = torch.empty(tuple(phi.shape), dtype=torch.float64, pin_memory=True)
+                    self.buf = torch.empty(tuple(phi.shape), dtype=dg.dtype, pin_memory=True)
                 else:
-                    b = torch.empty(tuple(phi.shape), dtype=torch.float64)
+                    b = torch.empty(tuple(phi.shape), dtype=dg.dtype)
                     b.zero_()  # first touch off the critical path
                     self.buf = b
 
@@ -199,7 +207,7 @@ def _host_mark_sources(grid, idx):
 class Workspace:
     def __init__(self, geom: _native.Geom, device: torch.device):
         n = C.c_size_t(0)
-        _native.check(_native.lib().eik_workspace_size(C.byref(geom), C.byref(n)))
+        _native.check(_native.lib(geom.dtype).eik_workspace_size(C.byref(geom), C.byref(n)), geom.dtype)
         self.nbytes = int(n.value)
         self.buf = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
         self.gen = 0  # bumped by every call that rewrites the remedy set slots
@@ -213,7 +221,7 @@ _WS: dict = {}
 
 
 def workspace(geom: _native.Geom, device: torch.device) -> Workspace:
-    key = (str(device), geom.nx, geom.ny, geom.nz, geom.ndim)
+    key = (str(device), geom.nx, geom.ny, geom.nz, geom.ndim, geom.dtype)
     ws = _WS.get(key)
     if ws is None:
         if len(_WS) >= 4:
@@ -338,13 +346,13 @@ def ifim_update_step(grid, bc, tol: float = 1e-12, workers: int = 1) -> RunStats
     hcap = _history_cap(geom)
     hist = np.zeros(hcap, dtype=np.int64)
     st = _native.Stats()
-    rc = _native.lib().eik_ifim_update_step(
+    rc = _native.lib(geom.dtype).eik_ifim_update_step(
         C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), _ptr(si), _ptr(sv), len(idx), float(tol),
         ws.ptr, ws.nbytes, hist.ctypes.data_as(C.c_void_p), hcap, C.byref(st), dg.stream)
     if dg.host:
         _host_mark_sources(grid, idx)
         dg.commit(phi=True)
-    _native.check(rc)
+    _native.check(rc, geom.dtype)
     d = _stats_from(st)
     stats = RunStats(active_history=hist[: d["upd_iterations"]].tolist())
     stats.iterations = d["upd_iterations"]
@@ -366,12 +374,12 @@ def build_remedy_set(grid, tol: float = 1e-12, workers: int = 1):
     ws = workspace(geom, dg.device)
     ws.gen += 1
     st = _native.Stats()
-    _native.check(_native.lib().eik_build_remedy(
+    _native.check(_native.lib(geom.dtype).eik_build_remedy(
         C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), float(tol), ws.ptr, ws.nbytes,
         C.byref(st), dg.stream))
     n = int(np.prod(tuple(int(s) for s in grid.phi.shape)))
     mask = torch.empty(n, dtype=torch.uint8, device=dg.device)
-    _native.check(_native.lib().eik_remedy_export(C.byref(geom), ws.ptr, ws.nbytes, _ptr(mask), dg.stream))
+    _native.check(_native.lib(geom.dtype).eik_remedy_export(C.byref(geom), ws.ptr, ws.nbytes, _ptr(mask), dg.stream))
     remedy = RemedySet(_device={"mask": mask, "count": int(st.remedy_size), "ws": ws, "gen": ws.gen,
                                 "host": dg.host, "shape": tuple(grid.phi.shape)})
     return remedy, int(st.build_calls)
@@ -388,14 +396,14 @@ def ifim_remedy_step(grid, remedy: RemedySet, tol: float = 1e-12, workers: int =
     if not fresh:
         mask = remedy._device_mask(tuple(grid.phi.shape), dg.device)
         cnt = C.c_int64(0)
-        _native.check(_native.lib().eik_remedy_load(C.byref(geom), _ptr(mask), _ptr(dg.state), ws.ptr, ws.nbytes,
+        _native.check(_native.lib(geom.dtype).eik_remedy_load(C.byref(geom), _ptr(mask), _ptr(dg.state), ws.ptr, ws.nbytes,
                                                     C.byref(cnt), dg.stream))
     ws.gen += 1
     st = _native.Stats()
-    rc = _native.lib().eik_remedy_step(C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), float(tol),
+    rc = _native.lib(geom.dtype).eik_remedy_step(C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), float(tol),
                                        ws.ptr, ws.nbytes, C.byref(st), dg.stream)
     dg.commit(phi=True)
-    _native.check(rc)
+    _native.check(rc, geom.dtype)
     remedy._drain()
     d = _stats_from(st)
     stats = RunStats()
@@ -424,6 +432,8 @@ def solve_ifim(grid, bc, tol: float = 1e-12, workers: int = 1, devices=None) -> 
     devs = resolve_devices(devices)
     idx, val = seed_linear(grid, bc)
     if devs is not None:
+        if field_dtype(grid) == _native.EIK_F32:
+            raise ValueError("the multi-device solve runs the float64 engine; pass float64 phi/speed")
         stats, phi = solve_multi(grid, idx, val, tol, devs)
         stats.wall_time = time.perf_counter() - t0
         return SolverResult(phi=phi, stats=stats)
@@ -437,14 +447,14 @@ def solve_ifim(grid, bc, tol: float = 1e-12, workers: int = 1, devices=None) -> 
     hist = np.zeros(hcap, dtype=np.int64)
     st = _native.Stats()
     out = _HostResult(dg)
-    rc = _native.lib().eik_ifim_solve(
+    rc = _native.lib(geom.dtype).eik_ifim_solve(
         C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), _ptr(si), _ptr(sv), len(idx), float(tol),
         ws.ptr, ws.nbytes, hist.ctypes.data_as(C.c_void_p), hcap, C.byref(st), dg.stream)
     phi = None
     if dg.host:
         _host_mark_sources(grid, idx)
         phi = out.commit()
-    _native.check(rc)
+    _native.check(rc, geom.dtype)
     d = _stats_from(st)
     stats = RunStats(
         iterations=d["iterations"],
