@@ -72,6 +72,7 @@ def lib():
         L.orc_build_remedy.argtypes = [GP, P, P, P, dbl, P, SP, C.c_int]
         L.orc_remedy_step.argtypes = [GP, P, P, P, P, dbl, P, i64, SP, C.c_int]
         L.orc_solve_ifim.argtypes = [GP, P, P, P, P, P, i64, dbl, P, i64, SP, P, C.c_int]
+        L.orc_solve_fim.argtypes = [GP, P, P, P, P, P, i64, dbl, SP]
         L.orc_solve_fixpoint.argtypes = [GP, P, P, P, P, P, i64, dbl, i64, SP, C.c_int]
         _lib = L
     return _lib
@@ -133,6 +134,25 @@ def solve_ifim(shape, spacing, speed, seed_idx, seed_val, state=None, phi=None, 
                         phases={"update": phases[0].as_dict(), "build": phases[1].as_dict(),
                                 "remedy": phases[2].as_dict()},
                         active_history=hist[: st.history_len].tolist())
+
+
+def solve_fim(shape, spacing, speed, seed_idx, seed_val, state=None, phi=None, tol=1e-12) -> OracleResult:
+    """Restatement of E/fim.py:62-144 (2D) and its 3D generalisation (serial)."""
+    g = geom(shape, spacing)
+    speed = np.ascontiguousarray(speed, dtype=np.float64).ravel()
+    n = speed.size
+    if state is None:
+        state = np.where(speed == 0.0, 4, 0).astype(np.uint8)
+    state = np.ascontiguousarray(state, dtype=np.uint8).ravel().copy()
+    phi = np.full(n, np.inf) if phi is None else np.ascontiguousarray(phi, dtype=np.float64).ravel().copy()
+    si = np.ascontiguousarray(seed_idx, dtype=np.int64)
+    sv = np.ascontiguousarray(seed_val, dtype=np.float64)
+    st = Stats()
+    rc = lib().orc_solve_fim(C.byref(g), _ptr(phi), _ptr(speed), _ptr(state), _ptr(si), _ptr(sv), si.size, tol,
+                             C.byref(st))
+    _check(rc, "solve_fim")
+    return OracleResult(phi=phi.reshape(shape), state=state.reshape(shape), stats=st.as_dict(), phases={},
+                        active_history=[])
 
 
 def update_step(shape, spacing, phi, speed, state, seed_idx, seed_val, tol=1e-12, threads=1):

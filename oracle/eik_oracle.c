@@ -16,6 +16,7 @@
  *   orc_build_remedy     <- E/ifim.py:137-161
  *   orc_remedy_step      <- E/ifim.py:164-218
  *   orc_solve_fixpoint   <- E/oracle.py:22-70
+ *   orc_solve_fim        <- E/fim.py:62-144 (FIM with per-iteration neighbour checks)
  *
  * 3D generalisation (the reference has no 3D engine): the same
  * engine with six axis neighbours, linear index (k*ny+j)*nx+i, local solver
@@ -547,6 +548,101 @@ int orc_solve_fixpoint(const orc_geom *g, double *phi, const double *speed, uint
 }
 
 /* Batch entry points used by the local-solver parity tests (per-element spacing). */
+/* ---- solve_fim: E/fim.py:62-144 (serial, the reference's list orders) ----
+ * Phase one: Jacobi values of the active list; settle (|v-old| <= tol) or write
+ * and survive (:95-108).  Phase two: every cell active this iteration examines
+ * its neighbours: skip fixed / ACTIVE, activate +inf ones, queue the others as
+ * checks -- one counted call per examination (:110-124).  Checks: Jacobi values
+ * from the post-phase-one field; a non-active check cell whose value drops by
+ * more than tol is written and re-activated (:126-138). */
+enum { F_FAR = 0, F_ACTIVE = 1, F_SETTLED = 2 }; /* E/fim.py:29 */
+
+int orc_solve_fim(const orc_geom *g, double *phi, const double *speed, uint8_t *state,
+                  const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol, orc_stats *st)
+{
+    if (!(tol > 0)) return ORC_EINVAL;
+    int rc = orc_apply_boundary(g, phi, state, seed_idx, seed_val, nseeds);
+    if (rc) return rc;
+    const int64_t n = ncells(g);
+    memset(st, 0, sizeof(*st));
+    const size_t cap_n = (size_t)(n > 0 ? n : 1);
+    uint8_t *label = (uint8_t *)calloc(cap_n, 1);
+    int64_t *active = (int64_t *)malloc(sizeof(int64_t) * cap_n);
+    int64_t *surv = (int64_t *)malloc(sizeof(int64_t) * cap_n);
+    int64_t *check = (int64_t *)malloc(sizeof(int64_t) * cap_n * 6);
+    double *values = (double *)malloc(sizeof(double) * cap_n * 6);
+    if (!label || !active || !surv || !check || !values) {
+        free(label); free(active); free(surv); free(check); free(values);
+        return ORC_ENOMEM;
+    }
+    int64_t na = 0, nb[6];
+    for (int64_t s = 0; s < nseeds; ++s) { /* :78-84 */
+        int m = neighbors(g, seed_idx[s], nb);
+        for (int q = 0; q < m; ++q) {
+            int64_t c = nb[q];
+            if (state[c] != ST_BLOCKED && state[c] != ST_SOURCE && label[c] == F_FAR) {
+                label[c] = F_ACTIVE;
+                active[na++] = c;
+            }
+        }
+    }
+    st->peak_active = na;
+    const int64_t cap = cap_of(g, 40);
+    rc = ORC_OK;
+    while (na > 0) {
+        st->iterations += 1;
+        if (st->iterations > cap) { rc = ORC_ECAP; break; }
+        batch_values(g, phi, speed, active, na, values, 1);
+        st->solver_calls += na;
+        int64_t ns = 0;
+        for (int64_t p = 0; p < na; ++p) {
+            int64_t c = active[p];
+            double v = values[p], old = phi[c];
+            if (v == old || fabs(v - old) <= tol) {
+                label[c] = F_SETTLED;
+            } else {
+                phi[c] = v;
+                st->phi_writes += 1;
+                surv[ns++] = c;
+            }
+        }
+        int64_t nc = 0;
+        for (int64_t p = 0; p < na; ++p) {
+            int m = neighbors(g, active[p], nb);
+            for (int q = 0; q < m; ++q) {
+                int64_t c = nb[q];
+                if (state[c] == ST_BLOCKED || state[c] == ST_SOURCE || label[c] == F_ACTIVE) continue;
+                if (phi[c] == INFINITY) {
+                    label[c] = F_ACTIVE;
+                    surv[ns++] = c;
+                } else {
+                    check[nc++] = c;
+                }
+            }
+        }
+        int64_t *t = active; active = surv; surv = t;
+        na = ns;
+        if (nc > 0) {
+            batch_values(g, phi, speed, check, nc, values, 1);
+            st->solver_calls += nc;
+            for (int64_t p = 0; p < nc; ++p) {
+                int64_t c = check[p];
+                if (label[c] == F_ACTIVE) continue;
+                double v = values[p];
+                if (v < phi[c] - tol) {
+                    phi[c] = v;
+                    st->phi_writes += 1;
+                    label[c] = F_ACTIVE;
+                    active[na++] = c;
+                }
+            }
+        }
+        if (na > st->peak_active) st->peak_active = na;
+    }
+    free(label); free(active); free(surv); free(check); free(values);
+    return rc;
+}
+
 void orc_update_2d_uniform_batch(const double *a, const double *b, const double *f, const double *delta,
                                  double *out, int64_t n)
 {

@@ -41,3 +41,13 @@ def local_vectors():
 @pytest.fixture(scope="session")
 def staged2d():
     return np.load(os.path.join(GOLDEN, "staged2d.npz"))
+
+
+@pytest.fixture(scope="session")
+def fim2d():
+    return load_cases("fim2d")
+
+
+@pytest.fixture(scope="session")
+def fim3d():
+    return load_cases("fim3d")

@@ -19,6 +19,9 @@ What it writes (all small, committed):
   reference outputs of update_2d_uniform / update_2d_aniso /
   update_3d_uniform (E/local_solver.py:39-157), plus the sha256 of all 100k
   3D outputs.
+* ``fim2d.json`` / ``fim3d.json`` (+ ``.npz`` phi) -- FIM (E/fim.py:62-144, SURVEY.md
+  §8f rank 3) on the inputs of cases2d / cases3d: the reference ``solve_fim`` in 2D,
+  ``fim3d_py`` (a literal 3D generalisation calling ``update_3d_uniform``) in 3D.
 * ``cases3d.npz`` + ``cases3d.json`` -- 3D engine cases.  The reference has no
   3D engine, so these come from ``ifim3d_py`` below: a literal
   3D generalisation of E/ifim.py that calls the reference's own scalar
@@ -39,6 +42,7 @@ sys.dont_write_bytecode = True
 sys.path.insert(0, REF)
 
 from eikonal.grid import BoundaryCondition, CellIndex, CellState, new_grid, seed_point  # noqa: E402
+from eikonal.fim import solve_fim  # noqa: E402
 from eikonal.harness import field_sha256, make_example  # noqa: E402
 from eikonal.ifim import build_remedy_set, ifim_remedy_step, ifim_update_step  # noqa: E402
 from eikonal.local_solver import update_2d_aniso, update_2d_uniform, update_3d_uniform  # noqa: E402
@@ -417,8 +421,99 @@ def write_cases_3d():
         json.dump(meta, fh, indent=1, sort_keys=True)
 
 
+def fim3d_py(nx, ny, nz, h, speed, state, seeds, tol=1e-12):
+    """E/fim.py:62-144 in 3D (six neighbours, update_3d_uniform). Returns (phi, stats)."""
+    n = nx * ny * nz
+    phi = np.full(n, INF)
+    state = state.copy()
+    for c, v in seeds:
+        phi[c] = v
+        state[c] = CellState.SOURCE
+    blocked = state == CellState.BLOCKED
+    seed = state == CellState.SOURCE
+    FAR, ACT, SET = 0, 1, 2
+    label = np.zeros(n, dtype=np.uint8)
+    active = []
+    for c, _ in seeds:
+        for nb in _nbrs3(c, nx, ny, nz):
+            if not blocked[nb] and not seed[nb] and label[nb] == FAR:
+                label[nb] = ACT
+                active.append(nb)
+    it, calls, peak = 0, 0, len(active)
+    cap = 40 * (nx + ny + nz)
+    while active:
+        it += 1
+        assert it <= cap
+        snap = phi.copy()
+        values = [_value3(snap, speed, c, nx, ny, nz, h) for c in active]
+        calls += len(active)
+        surv = []
+        for c, v in zip(active, values):
+            old = phi[c]
+            if v == old or abs(v - old) <= tol:
+                label[c] = SET
+            else:
+                phi[c] = v
+                surv.append(c)
+        check = []
+        for c in active:
+            for nb in _nbrs3(c, nx, ny, nz):
+                if blocked[nb] or seed[nb] or label[nb] == ACT:
+                    continue
+                if phi[nb] == INF:
+                    label[nb] = ACT
+                    surv.append(nb)
+                else:
+                    check.append(nb)
+        active = surv
+        if check:
+            snap = phi.copy()
+            values = [_value3(snap, speed, c, nx, ny, nz, h) for c in check]
+            calls += len(check)
+            for c, v in zip(check, values):
+                if label[c] == ACT:
+                    continue
+                if v < phi[c] - tol:
+                    phi[c] = v
+                    label[c] = ACT
+                    active.append(c)
+        peak = max(peak, len(active))
+    return phi, dict(iterations=it, solver_calls=calls, peak_active=peak,
+                     sha256=hashlib.sha256(phi.tobytes()).hexdigest())
+
+
+def write_fim():
+    meta2, arr2 = {}, {}
+    for name, (g, bc) in cases_2d().items():
+        r = solve_fim(g, bc)
+        st = r.stats
+        meta2[name] = dict(iterations=st.iterations, solver_calls=st.solver_calls, peak_active=st.peak_active,
+                           sha256=field_sha256(r.phi))
+        if g.nx * g.ny <= 64 * 96:
+            arr2[f"{name}__phi"] = r.phi
+        print("fim", name, st.iterations, st.solver_calls, st.peak_active)
+    np.savez_compressed(os.path.join(HERE, "fim2d.npz"), **arr2)
+    with open(os.path.join(HERE, "fim2d.json"), "w") as fh:
+        json.dump(meta2, fh, indent=1, sort_keys=True)
+    meta3, arr3 = {}, {}
+    for name, (nx, ny, nz, h, F, seeds) in cases_3d().items():
+        F = np.asarray(F, dtype=np.float64)
+        state = np.where(F == 0.0, CellState.BLOCKED, CellState.FAR).astype(np.uint8)
+        phi, st = fim3d_py(nx, ny, nz, h, F, state, seeds)
+        meta3[name] = st
+        arr3[f"{name}__phi"] = phi
+        print("fim3d", name, st["iterations"], st["solver_calls"], st["peak_active"])
+    np.savez_compressed(os.path.join(HERE, "fim3d.npz"), **arr3)
+    with open(os.path.join(HERE, "fim3d.json"), "w") as fh:
+        json.dump(meta3, fh, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["fim"]:
+        write_fim()
+        sys.exit(0)
     write_local_solver()
     write_staged_2d()
     write_cases_2d()
     write_cases_3d()
+    write_fim()

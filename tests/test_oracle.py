@@ -143,3 +143,42 @@ def test_oracle_vs_live_reference_random_grids():
         assert np.array_equal(bits(r.phi), bits(ref.phi))
         assert r.stats["solver_calls"] == ref.stats.solver_calls
         assert r.active_history == ref.stats.active_history
+
+
+def test_fim_2d_matches_reference_golden(cases2d, fim2d):
+    """orc_solve_fim (E/fim.py:62-144) vs the live reference solve_fim on the cases2d inputs."""
+    meta, Z = cases2d
+    fmeta, FZ = fim2d
+    for name, m in meta.items():
+        r = cpu.solve_fim((m["ny"], m["nx"]), (m["dx"], m["dy"]), Z[name + "__speed"], Z[name + "__seed_idx"],
+                          Z[name + "__seed_val"], state=Z[name + "__state0"])
+        f = fmeta[name]
+        assert sha(r.phi) == f["sha256"], name
+        assert (r.stats["iterations"], r.stats["solver_calls"], r.stats["peak_active"]) == (
+            f["iterations"], f["solver_calls"], f["peak_active"]), name
+
+
+def test_fim_3d_matches_golden(cases3d, fim3d):
+    meta, Z = cases3d
+    fmeta, FZ = fim3d
+    for name, m in meta.items():
+        r = cpu.solve_fim((m["nz"], m["ny"], m["nx"]), m["h"], Z[name + "__speed"], Z[name + "__seed_idx"],
+                          Z[name + "__seed_val"], state=Z[name + "__state0"])
+        f = fmeta[name]
+        assert sha(r.phi) == f["sha256"], name
+        assert (r.stats["iterations"], r.stats["solver_calls"], r.stats["peak_active"]) == (
+            f["iterations"], f["solver_calls"], f["peak_active"]), name
+
+
+def test_fim_and_ifim_agree_on_the_fixpoint(cases2d):
+    """T/test_fim.py:18-24: FIM and iFIM both reach the fixpoint field (within 1e-9)."""
+    meta, Z = cases2d
+    for name in ("ex2_48", "ex5_48", "pocket_24", "checker_64"):
+        m = meta[name]
+        args = ((m["ny"], m["nx"]), (m["dx"], m["dy"]), Z[name + "__speed"], Z[name + "__seed_idx"],
+                Z[name + "__seed_val"])
+        a = cpu.solve_fim(*args, state=Z[name + "__state0"]).phi
+        b = cpu.solve_ifim(*args, state=Z[name + "__state0"]).phi
+        fin = np.isfinite(b)
+        assert np.array_equal(np.isfinite(a), fin)
+        assert np.abs(a[fin] - b[fin]).max() <= 1e-9, name
