@@ -122,6 +122,13 @@ int eik_solve_fixpoint(const eik_geom *g, double *phi, const double *speed, uint
                        const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
                        int64_t max_passes, void *workspace, size_t workspace_bytes, eik_stats *out, void *stream);
 
+/* solve_fim (E/fim.py:62-144): the FIM baseline with
+ * per-iteration neighbour checks.  out: iterations, solver_calls (active
+ * recomputations + one per neighbour examination), peak_active, phi_writes. */
+int eik_solve_fim(const eik_geom *g, double *phi, const double *speed, uint8_t *state, const int64_t *seed_idx,
+                  const double *seed_val, int64_t nseeds, double tol, void *workspace, size_t workspace_bytes,
+                  eik_stats *out, void *stream);
+
 /* max_residual (E/harness.py:147-162): largest |phi - U(phi)| over free cells with finite phi. */
 int eik_max_residual(const eik_geom *g, const double *phi, const double *speed, const uint8_t *state,
                      void *workspace, size_t workspace_bytes, double *out, void *stream);
@@ -209,6 +216,9 @@ int eik_ifim_solve_f32(const eik_geom *g, float *phi, const float *speed, uint8_
 int eik_solve_fixpoint_f32(const eik_geom *g, float *phi, const float *speed, uint8_t *state,
                            const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
                            int64_t max_passes, void *workspace, size_t workspace_bytes, eik_stats *out, void *stream);
+int eik_solve_fim_f32(const eik_geom *g, float *phi, const float *speed, uint8_t *state, const int64_t *seed_idx,
+                      const double *seed_val, int64_t nseeds, double tol, void *workspace, size_t workspace_bytes,
+                      eik_stats *out, void *stream);
 int eik_max_residual_f32(const eik_geom *g, const float *phi, const float *speed, const uint8_t *state,
                          void *workspace, size_t workspace_bytes, double *out, void *stream);
 int eik_local_solve_f32(int kind, const float *a, const float *b, const float *c, const float *f, double dx,

@@ -20,6 +20,7 @@ from .grid import (
     seed_linear,
     seed_point,
 )
+from .fim import solve_fim
 from .fixpoint import max_residual, solve_fixpoint
 from .harness import METHOD_NAMES, PARALLEL_METHODS, field_max_diff, field_sha256, run_method
 from .ifim import (
@@ -39,6 +40,6 @@ __all__ = [
     "INF", "BoundaryCondition", "CellIndex", "CellIndex3D", "CellState", "Grid", "Grid3D", "METHOD_NAMES",
     "PARALLEL_METHODS", "RemedySet", "RunStats", "SolverResult", "build_remedy_set", "clear_workspaces",
     "field_max_diff", "field_sha256", "ifim_remedy_step", "ifim_update_step", "new_grid", "new_grid_3d",
-    "reset_field", "resolve_workers", "run_method", "seed_linear", "seed_point", "solve_ifim", "solve_fixpoint",
+    "reset_field", "resolve_workers", "run_method", "seed_linear", "seed_point", "solve_fim", "solve_ifim", "solve_fixpoint",
     "max_residual",
 ]

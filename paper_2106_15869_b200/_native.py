@@ -34,7 +34,7 @@ EXPORTS = (
     "eik_remedy_export", "eik_remedy_step", "eik_ifim_solve", "eik_local_solve",
     "eik_last_error", "eik_version", "eik_workspace_offsets", "eik_slab_update_init", "eik_slab_update_iter",
     "eik_slab_apply_requests", "eik_slab_build", "eik_slab_remedy_round", "eik_solve_fixpoint",
-    "eik_max_residual", "eik_mr_prepare", "eik_mr_run", "eik_peer_enable",
+    "eik_max_residual", "eik_mr_prepare", "eik_mr_run", "eik_peer_enable", "eik_solve_fim",
 )
 
 
@@ -91,7 +91,7 @@ class Stats(C.Structure):
 EXPORTS_F32 = (
     "eik_workspace_size_f32", "eik_ifim_update_step_f32", "eik_build_remedy_f32", "eik_remedy_load_f32",
     "eik_remedy_export_f32", "eik_remedy_step_f32", "eik_ifim_solve_f32", "eik_solve_fixpoint_f32",
-    "eik_max_residual_f32", "eik_local_solve_f32", "eik_last_error_f32", "eik_version_f32",
+    "eik_max_residual_f32", "eik_local_solve_f32", "eik_last_error_f32", "eik_version_f32", "eik_solve_fim_f32",
 )
 
 _lib = None
@@ -140,6 +140,7 @@ def lib(dtype: int = EIK_F64):
     L.eik_slab_remedy_round.argtypes = [GP, P, P, P, dbl, i64, P, C.c_size_t, C.POINTER(i64), C.POINTER(i64), vp]
     L.eik_solve_fixpoint.argtypes = [GP, P, P, P, P, P, i64, dbl, i64, P, C.c_size_t, SP, vp]
     L.eik_max_residual.argtypes = [GP, P, P, P, P, C.c_size_t, C.POINTER(dbl), vp]
+    L.eik_solve_fim.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, SP, vp]
     RP = C.POINTER(Rank)
     L.eik_mr_prepare.argtypes = [GP, C.c_int32, RP, C.c_int32, C.c_int32, P, P, P, P, i64, dbl, vp]
     L.eik_mr_run.argtypes = [GP, C.c_int32, RP, C.c_int32, C.c_int32, P, P, dbl, P, i64, SP, vp]
@@ -168,6 +169,7 @@ def _lib_f32():
     L.eik_ifim_solve_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]
     L.eik_solve_fixpoint_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, i64, P, C.c_size_t, SP, vp]
     L.eik_max_residual_f32.argtypes = [GP, P, P, P, P, C.c_size_t, C.POINTER(dbl), vp]
+    L.eik_solve_fim_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, SP, vp]
     L.eik_local_solve_f32.argtypes = [C.c_int, P, P, P, P, dbl, dbl, P, i64, vp]
     L.eik_last_error_f32.restype = C.c_char_p
     L.eik_version_f32.restype = C.c_char_p

@@ -106,6 +106,7 @@ struct Ctl {
     unsigned long long nz_sectors;
     unsigned wcount;                // multi-rank: world-barrier arrivals (rank 0's copy is used)
     unsigned wgen;                  // multi-rank: this rank's world-barrier generation
+    unsigned fc[3];                 // FIM: check-list length per rotating slot
 #ifdef EIK_DIAG
     unsigned long long dg[4][26];   // remedy rounds by log2|R_r|: count, phase B ns, phase A ns, members
 #endif
@@ -170,6 +171,7 @@ struct KP {
     const uint8_t *state;
     uint32_t *Bt;                 // touched bitmap (update step labels: not FAR)
     uint32_t *L0, *L1;            // update-step cell worklists
+    uint32_t *L2;                 // FIM: check list
     Ctl *ctl;
     int64_t *hist;
     int64_t hist_cap;
@@ -1464,6 +1466,205 @@ __global__ void __launch_bounds__(BLOCK) k_fixpoint(KP p)
     }
 }
 
+// ---------------------------------------------------------------------------
+// FIM (E/fim.py:62-144): the paper's baseline, with the
+// per-iteration neighbour checks iFIM drops.  One persistent launch, five
+// grid barriers per iteration, phi updated in place between them:
+//   1  values of the active list from the snapshot (stored per list slot)
+//   2  settle (|v-old| <= tol -> SETTLED) or write and survive (:95-108)
+//   3  every cell active this iteration examines its neighbours: fixed and
+//      ACTIVE ones are skipped, +inf ones are activated once (claim bitmap),
+//      finite ones are checks -- one counted call per examination, computed
+//      once per distinct cell (:110-124)
+//   4  values of the distinct checks from the post-phase-2 field
+//   5  a check that drops by more than tol is written and re-activated (:126-138)
+// Labels live in the palette-index buffer (unused by FIM), the claim bitmap in
+// the R0 slot; both are cleared by the host before the launch.
+// ---------------------------------------------------------------------------
+constexpr uint8_t FIM_ACTIVE = 1, FIM_SETTLED = 2;  // E/fim.py:29 (FAR = 0)
+
+template <int DIM, int SOL>
+__device__ __forceinline__ real_t cell_solve(const KP &p, const real_t *P, uint32_t c, uint32_t x, uint32_t y,
+                                             uint32_t z)
+{
+    Sten t;
+    t.c = __ldcg(P + c);
+    t.w = x > 0 ? __ldcg(P + c - 1) : INFINITY;
+    t.e = x + 1 < (uint32_t)p.nx ? __ldcg(P + c + 1) : INFINITY;
+    t.s = y > 0 ? __ldcg(P + c - p.nx32) : INFINITY;
+    t.n = y + 1 < (uint32_t)p.ny ? __ldcg(P + c + p.nx32) : INFINITY;
+    t.d = t.u = INFINITY;
+    if (DIM == 3) {
+        t.d = z > 0 ? __ldcg(P + c - p.plane32) : INFINITY;
+        t.u = z + 1 < (uint32_t)p.nz ? __ldcg(P + c + p.plane32) : INFINITY;
+    }
+    t.k = coef<SOL>(p, false, c);
+    return solve<DIM, SOL>(p, t);
+}
+
+template <int DIM>
+__device__ __forceinline__ void cell_xyz(const KP &p, uint32_t c, uint32_t &x, uint32_t &y, uint32_t &z, uint32_t &row)
+{
+    row = fdiv(c, p.fnx);
+    x = c - row * p.nx32;
+    if (DIM == 3) {
+        z = fdiv(row, p.fny);
+        y = row - z * (uint32_t)p.ny;
+    } else {
+        z = 0;
+        y = row;
+    }
+}
+
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK) k_fim(KP p)
+{
+    __shared__ unsigned sscan[WPB + 1];
+    __shared__ unsigned long long sred[WPB];
+    Ctl *ctl = p.ctl;
+    real_t *P = p.P0;
+    real_t *V = p.P1;       // values per list slot (phases 1 and 4)
+    uint8_t *lab = p.pidx;  // FIM labels
+    uint32_t *claim = p.R0b;
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nthr = gridDim.x * blockDim.x;
+    const uint32_t bstride = gridDim.x * BLOCK;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned nA = vload(&ctl->len[0]);  // initial Active (k_init_active, E/fim.py:78-84)
+    for (uint32_t i = tid; i < nA; i += nthr) lab[__ldcg(p.L0 + i)] = FIM_ACTIVE;
+    if (lead) {
+        ctl->peak = nA;
+        ctl->sum = 0;
+    }
+    if (!grid_barrier(ctl)) return;
+    for (int64_t it = 0; nA > 0; ++it) {
+        if (it >= p.cap) {  // E/fim.py:90-92
+            if (lead) ctl->err = EIK_ECAP;
+            return;
+        }
+        const uint32_t *LA = (it & 1) ? p.L1 : p.L0;
+        uint32_t *LN = (it & 1) ? p.L0 : p.L1;
+        unsigned *lenN = &ctl->len[(it + 1) % 3];
+        unsigned *lenC = &ctl->fc[it % 3];
+        if (lead) {
+            ctl->len[(it + 2) % 3] = 0;
+            ctl->fc[(it + 1) % 3] = 0;
+            ctl->iters = (unsigned long long)(it + 1);
+            ctl->sum += nA;
+        }
+        // 1: values from the snapshot; clear the claims of last iteration's activations
+        for (uint32_t i = tid; i < nA; i += nthr) {
+            const uint32_t c = __ldcg(LA + i);
+            uint32_t x, y, z, row;
+            cell_xyz<DIM>(p, c, x, y, z, row);
+            V[i] = cell_solve<DIM, SOL>(p, P, c, x, y, z);
+            atomicAnd(claim + row * p.W + (x >> 5), ~(1u << (x & 31)));
+        }
+        if (!grid_barrier(ctl)) return;
+        // 2: settle or write and survive
+        unsigned long long wr = 0;
+        for (uint32_t base = blockIdx.x * BLOCK; base < nA; base += bstride) {
+            const uint32_t i = base + threadIdx.x;
+            unsigned stay = 0;
+            uint32_t c = 0;
+            if (i < nA) {
+                c = __ldcg(LA + i);
+                const real_t v = V[i], old = __ldcg(P + c);
+                if (v == old || fabs(v - old) <= tol_at(p.tol, old)) {
+                    lab[c] = FIM_SETTLED;
+                } else {
+                    P[c] = v;
+                    stay = 1;
+                    ++wr;
+                }
+            }
+            const unsigned pos = block_reserve(stay, lenN, sscan);
+            if (stay) LN[pos] = c;
+        }
+        if (!grid_barrier(ctl)) return;
+        // 3: neighbour examination
+        unsigned long long pairs = 0;
+        for (uint32_t base = blockIdx.x * BLOCK; base < nA; base += bstride) {
+            const uint32_t i = base + threadIdx.x;
+            uint32_t act[6], chk[6];
+            unsigned na = 0, nc = 0;
+            if (i < nA) {
+                const uint32_t c = __ldcg(LA + i);
+                uint32_t x, y, z, row;
+                cell_xyz<DIM>(p, c, x, y, z, row);
+#pragma unroll
+                for (int k = 0; k < (DIM == 3 ? 6 : 4); ++k) {
+                    const bool inb = k == 0 ? x > 0 : k == 1 ? x + 1 < p.nx32 : k == 2 ? y > 0
+                                     : k == 3 ? y + 1 < (uint32_t)p.ny : k == 4 ? z > 0 : z + 1 < (uint32_t)p.nz;
+                    if (!inb) continue;
+                    const uint32_t e = k == 0 ? c - 1 : k == 1 ? c + 1 : k == 2 ? c - p.nx32 : k == 3 ? c + p.nx32
+                                       : k == 4 ? c - p.plane32 : c + p.plane32;
+                    const uint32_t xe = k == 0 ? x - 1 : k == 1 ? x + 1 : x;
+                    const uint32_t re = k == 2 ? row - 1 : k == 3 ? row + 1 : k == 4 ? row - (uint32_t)p.ny
+                                        : k == 5 ? row + (uint32_t)p.ny : row;
+                    const uint32_t w = re * p.W + (xe >> 5), bit = 1u << (xe & 31);
+                    if (__ldg(p.Fb + w) & bit) continue;  // blocked or seed
+                    if (*(volatile uint8_t *)(lab + e) == FIM_ACTIVE) continue;
+                    const bool unreached = __ldcg(P + e) == INFINITY;
+                    if (!unreached) ++pairs;  // one counted call per examination (E/fim.py:124)
+                    if (atomicOr(claim + w, bit) & bit) continue;
+                    if (unreached) {
+                        lab[e] = FIM_ACTIVE;
+                        act[na++] = e;
+                    } else {
+                        chk[nc++] = e;
+                    }
+                }
+            }
+            unsigned pos = block_reserve(na, lenN, sscan);
+            for (unsigned q = 0; q < na; ++q) LN[pos + q] = act[q];
+            pos = block_reserve(nc, lenC, sscan);
+            for (unsigned q = 0; q < nc; ++q) p.L2[pos + q] = chk[q];
+        }
+        {
+            const unsigned long long t = block_sum(pairs, sred);
+            if (threadIdx.x == 0 && t) atomicAdd(&ctl->sum, t);
+        }
+        if (!grid_barrier(ctl)) return;
+        // 4: values of the distinct checks from the post-phase-2 field
+        const unsigned nC = vload(lenC);
+        for (uint32_t j = tid; j < nC; j += nthr) {
+            const uint32_t c = __ldcg(p.L2 + j);
+            uint32_t x, y, z, row;
+            cell_xyz<DIM>(p, c, x, y, z, row);
+            V[j] = cell_solve<DIM, SOL>(p, P, c, x, y, z);
+        }
+        if (!grid_barrier(ctl)) return;
+        // 5: re-activate checks that dropped by more than tol
+        for (uint32_t base = blockIdx.x * BLOCK; base < nC; base += bstride) {
+            const uint32_t j = base + threadIdx.x;
+            unsigned go = 0;
+            uint32_t c = 0;
+            if (j < nC) {
+                c = __ldcg(p.L2 + j);
+                uint32_t x, y, z, row;
+                cell_xyz<DIM>(p, c, x, y, z, row);
+                atomicAnd(claim + row * p.W + (x >> 5), ~(1u << (x & 31)));
+                const real_t v = V[j], old = __ldcg(P + c);
+                if (v < old - tol_at(p.tol, old)) {  // E/fim.py:135
+                    P[c] = v;
+                    lab[c] = FIM_ACTIVE;
+                    go = 1;
+                    ++wr;
+                }
+            }
+            const unsigned pos = block_reserve(go, lenN, sscan);
+            if (go) LN[pos] = c;
+        }
+        {
+            const unsigned long long t = block_sum(wr, sred);
+            if (threadIdx.x == 0 && t) atomicAdd(&ctl->writes, t);
+        }
+        if (!grid_barrier(ctl)) return;
+        nA = vload(lenN);
+        if (lead && nA > ctl->peak) ctl->peak = nA;
+    }
+}
+
 // max_residual (E/harness.py:147-162): max |phi - U(phi)| over free cells with
 // finite phi; result as IEEE bits in ctl->peak.
 template <int DIM, int SOL>
@@ -1559,7 +1760,7 @@ size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 struct Layout {
     int64_t N;
     uint32_t W, nwords, npos, nty4, ntt;
-    size_t off_phi2, off_dd, off_bt, off_l0, off_l1;
+    size_t off_phi2, off_dd, off_bt, off_l0, off_l1, off_l2;
     size_t off_r0, off_d0, off_d1, off_f, off_pidx, off_ptab, off_phash, off_pslot, off_pstate;
     size_t off_hist, off_ctl_u, off_ctl_r, off_kps, total;
     int64_t cap_upd, cap_rem;
@@ -1595,6 +1796,7 @@ int make_layout(const eik_geom *g, Layout &L)
     L.off_bt = o; o += al(bm);
     L.off_l0 = o; o += al((size_t)L.N * 4);  // update: active cells; remedy: members
     L.off_l1 = o; o += al((size_t)L.N * 4);
+    L.off_l2 = o; o += al((size_t)L.N * 4);  // FIM check list
     L.off_r0 = o; o += al(bm);
     L.off_d0 = o; o += al(bm);
     L.off_d1 = o; o += al(bm);
@@ -1657,6 +1859,7 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, real_t *phi, const real
     p.Bt = (uint32_t *)(b + L.off_bt);
     p.L0 = (uint32_t *)(b + L.off_l0);
     p.L1 = (uint32_t *)(b + L.off_l1);
+    p.L2 = (uint32_t *)(b + L.off_l2);
     p.ctl = ctl;
     p.hist = (int64_t *)(b + L.off_hist);
     p.hist_cap = L.cap_upd + 2;
@@ -1812,6 +2015,10 @@ struct Engine {
     {
         return coop_launch(k_fixpoint<DIM, SOL>, p, nullptr, false, st, "EIK_FIX_BLOCKS_PER_SM", 0);
     }
+    static int fim(KP &p, cudaStream_t st)
+    {
+        return coop_launch(k_fim<DIM, SOL>, p, nullptr, false, st, "EIK_FIM_BLOCKS_PER_SM", 0);
+    }
     static int residual(KP &p, cudaStream_t st)
     {
         k_residual<DIM, SOL><<<stream_grid(p.nwords), BLOCK, 0, st>>>(p);
@@ -1900,7 +2107,7 @@ void fill_update_stats(const Ctl &c, eik_stats *o)
 int expose_latest(const Layout &L, const Ctl &c, real_t *phi, const real_t *phi2, cudaStream_t st)
 {
     if (c.iters & 1) {  // the newest values sit in the workspace buffer
-        CK(cudaMemcpyAsync(phi, phi2, (size_t)L.N * 8, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(phi, phi2, (size_t)L.N * sizeof(real_t), cudaMemcpyDeviceToDevice, st));
         CK(cudaStreamSynchronize(st));
     }
     return EIK_OK;
@@ -2207,7 +2414,7 @@ int EIK_FN(eik_solve_fixpoint)(const eik_geom *g, real_t *phi, const real_t *spe
     CK(cudaStreamSynchronize(st));
     if ((rc = check_hang(c, "fixpoint"))) return rc;
     if (c.iters & 1) {  // the last pass wrote the workspace buffer
-        CK(cudaMemcpyAsync(phi, p.P1, (size_t)L.N * 8, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(phi, p.P1, (size_t)L.N * sizeof(real_t), cudaMemcpyDeviceToDevice, st));
         CK(cudaStreamSynchronize(st));
     }
     int64_t nfree = 0;
@@ -2224,6 +2431,54 @@ int EIK_FN(eik_solve_fixpoint)(const eik_geom *g, real_t *phi, const real_t *spe
     out->total_ms = ev.ms(0, 1);
     out->gpu_launches = 3;
     if (c.err == EIK_ECAP) return fail(EIK_ECAP, "fixpoint iteration did not converge within %lld passes", (long long)cap);
+    return EIK_OK;
+}
+
+int EIK_FN(eik_solve_fim)(const eik_geom *g, real_t *phi, const real_t *speed, uint8_t *state,
+                          const int64_t *seed_idx, const double *seed_val, int64_t nseeds, double tol,
+                          void *workspace, size_t workspace_bytes, eik_stats *out, void *stream)
+{
+    Layout L;
+    int rc = make_layout(g, L);
+    if (rc) return rc;
+    if ((rc = check_ws(L, workspace, workspace_bytes))) return rc;
+    if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);  // E/fim.py:64-65
+    if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
+    if (nseeds < 1 || !seed_idx || !seed_val) return fail(EIK_EINVAL, "boundary condition has no seeds");
+    cudaStream_t st = (cudaStream_t)stream;
+    memset(out, 0, sizeof(*out));
+    char *b = (char *)workspace;
+    Ctl *ctl = (Ctl *)(b + L.off_ctl_u);
+    Events ev;
+    ev.rec(0, st);
+    CK(cudaMemsetAsync(ctl, 0, sizeof(Ctl), st));
+    k_seed<<<(int)std::min<int64_t>((nseeds + 255) / 256, 1024), 256, 0, st>>>(phi, state, seed_idx, seed_val, nseeds);
+    CK(cudaGetLastError());
+    KP p = make_kp(g, L, workspace, phi, speed, state, tol, ctl, L.cap_upd);
+    rc = dispatch(g, [&](auto E) {
+        int r = E.prep(p, false, true, st);
+        if (r) return r;
+        CK(cudaMemsetAsync(p.pidx, 0, (size_t)L.N, st));          // labels: FAR (after prep: palette slot)
+        CK(cudaMemsetAsync(p.R0b, 0, (size_t)L.nwords * 4, st));  // claims
+        r = E.init_active(p, seed_idx, nseeds, st);
+        if (r) return r;
+        return E.fim(p, st);
+    });
+    if (rc) return rc;
+    ev.rec(1, st);
+    Ctl c;
+    CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if ((rc = check_hang(c, "fim"))) return rc;
+    out->iterations = (int64_t)c.iters;
+    out->upd_iterations = (int64_t)c.iters;
+    out->solver_calls = out->upd_calls = (int64_t)c.sum;
+    out->peak_active = (int64_t)c.peak;
+    out->phi_writes = (int64_t)c.writes;
+    out->total_ms = out->upd_ms = ev.ms(0, 1);
+    out->gpu_launches = 5;
+    if (c.err == EIK_ECAP)
+        return fail(EIK_ECAP, "active list did not drain within %lld iterations", (long long)L.cap_upd);
     return EIK_OK;
 }
 

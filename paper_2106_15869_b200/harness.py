@@ -1,9 +1,10 @@
 """Dispatch and parity helpers for the iFIM path (E/harness.py:54-57, 121-179).
 
 ``run_method`` keeps the reference's string dispatch (the plugin point every
-CLI command goes through, E/harness.py:121-144).  "ifim" and "oracle" (the
-fixpoint ground truth, E/oracle.py) are served by this package; fmm, fsm and
-fim are out of scope and raise like an unknown method would.
+CLI command goes through, E/harness.py:121-144).  "ifim", "fim" (the paper's
+baseline, E/fim.py) and "oracle" (the fixpoint ground truth, E/oracle.py) are
+served by this package; fmm and fsm are out of scope and raise
+like an unknown method would.
 """
 from __future__ import annotations
 
@@ -12,16 +13,19 @@ import hashlib
 import numpy as np
 import torch
 
+from .fim import solve_fim
 from .fixpoint import max_residual, solve_fixpoint  # noqa: F401  (re-exported)
 from .ifim import solve_ifim
 from .result import SolverResult
 
-METHOD_NAMES = ("ifim", "oracle")
-PARALLEL_METHODS = frozenset({"ifim", "oracle"})
+METHOD_NAMES = ("fim", "ifim", "oracle")
+PARALLEL_METHODS = frozenset({"fim", "ifim", "oracle"})
 
 
 def run_method(method: str, grid, bc, tol: float = 1e-12, workers: int = 1) -> SolverResult:
     """E/harness.py:121-144 restricted to the accelerated method."""
+    if method == "fim":
+        return solve_fim(grid, bc, tol=tol, workers=workers)
     if method == "ifim":
         return solve_ifim(grid, bc, tol=tol, workers=workers)
     if method == "oracle":

@@ -83,7 +83,7 @@ def test_run_method_dispatch():
     g = eik.new_grid(4, 4, 1.0, 1.0)
     with pytest.raises(ValueError):
         eik.run_method("fmm", g, eik.seed_point(g, (0, 0), 0.0))
-    assert eik.METHOD_NAMES == ("ifim", "oracle")
+    assert eik.METHOD_NAMES == ("fim", "ifim", "oracle")
 
 
 def test_field_helpers_match_reference_semantics():
