@@ -265,6 +265,26 @@ class StepStats:
         self.launches, self.phase_ms = launches, phase_ms
 
 
+def make_fim_step(eik, torch, dev, w, dtype):
+    """One device-resident solve_fim (the paper's FIM baseline, E/fim.py) of the whole grid.
+    Its whole persistent kernel stands in for the roofline kernel: bytes = 8 x (2 calls + writes)."""
+    n, F = w.n, w.F.to(dtype)
+    phi0 = torch.full((n, n, n), float("inf"), dtype=dtype, device=dev)
+    st0 = torch.zeros((n, n, n), dtype=torch.uint8, device=dev)
+    phi, st = torch.empty_like(phi0), torch.empty_like(st0)
+    g = eik.Grid3D(n, n, n, w.h, (0.0, 0.0, 0.0), phi, F, st)
+    bc = eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in w.seeds))
+
+    def step():
+        phi.copy_(phi0)
+        st.copy_(st0)
+        s = eik.solve_fim(g, bc).stats
+        return StepStats(s.solver_calls, s.iterations, 0, s.solver_calls, s.phi_writes, s.device_ms["total"],
+                         s.gpu_launches, {"fim": round(s.device_ms["total"], 3)})
+
+    return step
+
+
 def make_single_step(eik, torch, dev, w, dtype):
     """One device-resident solve_ifim of the whole grid (inputs restored in the step)."""
     n, F = w.n, w.F.to(dtype)
@@ -376,14 +396,16 @@ def run_ours(args):
     workload = w.desc
     rdt = torch.float32 if args.dtype == "f32" else torch.float64
     rsize = 4 if args.dtype == "f32" else 8
-    if args.dtype == "f32" and (world > 1 or args.slabs):
-        raise SystemExit("the float32 perf mode is single-device")
+    if (args.dtype == "f32" or args.method == "fim") and (world > 1 or args.slabs):
+        raise SystemExit("the float32 perf mode and the FIM baseline are single-device")
     slabs = world > 1 or args.slabs
     mode = "single"
     if world > 1 and not args.host_slabs and peer_slabs_possible(torch, dev, world, local):
         step, mode = make_peer_step(torch, dev, w, world, rank), "peer"
     elif slabs:
         step, mode = make_slab_step(torch, dev, w, world, rank), "host"
+    elif args.method == "fim":
+        step = make_fim_step(eik, torch, dev, w, rdt)
     else:
         step = make_single_step(eik, torch, dev, w, rdt)
 
@@ -430,11 +452,11 @@ def run_ours(args):
     if mode == "peer":
         peak, peak_src = peak * world, peak_src + f" x {world} ranks"
     achieved = alg_bytes / rem_s / 1e9 if rem_s > 0 else None
-    traffic = traffic_from_profiles(workload) if not slabs and args.dtype == "f64" else None
+    traffic = traffic_from_profiles(workload) if not slabs and args.dtype == "f64" and args.method == "ifim" else None
 
     out = None
     if rank == 0:
-        e2e = run_e2e(eik, torch, dev, w, calls, args, rdt) if not (slabs or args.no_e2e) else \
+        e2e = run_e2e(eik, torch, dev, w, calls, args, rdt) if not (slabs or args.no_e2e or args.method == "fim") else \
             {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
              "note": "e2e is measured by the single-GPU run through solve_ifim"}
         cpu_calls, cpu_s = cpu_sample(args.cpu_size, os.cpu_count() or 1, args.config) if not args.no_cpu \
@@ -444,7 +466,7 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "strong" if slabs else "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": workload, "size": n, "solver_calls_per_step": calls,
+            "config": {"workload": workload, "size": n, "method": args.method, "solver_calls_per_step": calls,
                        "iterations": r.iterations, "peak_remedy": r.peak_remedy,
                        "parallelism": {"peer": f"z-slabs x{world} (peer-memory fused kernels)",
                                        "host": f"z-slabs x{world} (host-driven exchange)"}.get(mode, "single"),
@@ -453,7 +475,8 @@ def run_ours(args):
             "wall_clock_to_convergence_ms": ms / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "k_remedy", "alg_bytes_per_launch": alg_bytes, "launch_ms": rem_s * 1e3,
+                         "kernel": "k_fim" if args.method == "fim" else "k_remedy", "alg_bytes_per_launch": alg_bytes,
+                         "launch_ms": rem_s * 1e3,
                          "peak_source": peak_src},
             "cpu_baseline": {"value": (cpu_calls / cpu_s) if cpu_s else None, "unit": UNIT,
                              "cores": os.cpu_count() or 1, "kind": "port",
@@ -516,6 +539,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--method", default="ifim", choices=["ifim", "fim"],
+                    help="ifim = the accelerated path (headline); fim = the paper's FIM baseline on the GPU")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"],
                     help="f64 = parity mode (default, bit-exact); f32 = perf mode (max-rel 1e-5)")
     ap.add_argument("--slabs", action="store_true", help="use the z-slab protocol even on one GPU")
