@@ -401,7 +401,19 @@ def run_ours(args):
     slabs = world > 1 or args.slabs
     mode = "single"
     if world > 1 and not args.host_slabs and peer_slabs_possible(torch, dev, world, local):
-        step, mode = make_peer_step(torch, dev, w, world, rank), "peer"
+        import torch.distributed as dist
+
+        try:  # symmetric-memory slabs + one probe solve; any rank failing sends every rank to the NCCL path
+            step, mode = make_peer_step(torch, dev, w, world, rank), "peer"
+            step()
+            ok = 1
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] peer-memory slabs unavailable on rank {rank}: {e!r}", file=sys.stderr, flush=True)
+            ok = 0
+        t = torch.tensor([ok], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if not t.item():
+            step, mode = make_slab_step(torch, dev, w, world, rank), "host"
     elif slabs:
         step, mode = make_slab_step(torch, dev, w, world, rank), "host"
     elif args.method == "fim":
