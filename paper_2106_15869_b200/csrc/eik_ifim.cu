@@ -1100,9 +1100,6 @@ constexpr int REM_PER = 4;  // bitmap words per thread in phase B
 #ifndef REM_MU
 #define REM_MU 2            // phase A: members per lane in flight
 #endif
-#ifndef REM_PREF
-#define REM_PREF 0          // phase A: 1 = list entries one iteration ahead, 2 = + L2 prefetch of their rows
-#endif
 
 
 template <int DIM, bool MR>
@@ -1157,12 +1154,6 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
                 }
                 Dc[w] = 0;  // D_r is accumulated by phase A with atomicOr
                 cnt += __popc(R[k]);
-#ifdef EIK_DIAG_SECT
-                if (R[k]) {
-                    atomicAdd(&p.ctl->nz_words, 1ull);
-                    atomicAdd(&p.ctl->nz_sectors, (unsigned long long)__popc((R[k] | (R[k] >> 1) | (R[k] >> 2) | (R[k] >> 3)) & 0x11111111u));
-                }
-#endif
             }
         }
         unsigned pos = block_reserve(cnt, lenR, sscan);
@@ -1255,22 +1246,10 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
         }
         // ---- phase A: one local solve per member, REM_MU members per lane in flight ----
         unsigned long long a_dec = 0;
-#ifdef REM_GRIDSTRIDE
-        const uint32_t wbase = ((gb * BLOCK + threadIdx.x) - lane) * REM_MU, wstride = gnb * BLOCK * REM_MU, mend = m;
-#else
         // one contiguous segment of the (brick-ordered) list per CTA: L1 reuse of neighbour rows
         const uint32_t seg = ((m + gnb - 1) / gnb + 32 * REM_MU - 1) / (32 * REM_MU) * (32 * REM_MU);
         const uint32_t sbeg = gb * seg, mend = min(m, sbeg + seg);
         const uint32_t wbase = sbeg + (threadIdx.x >> 5) * 32 * REM_MU, wstride = WPB * 32 * REM_MU;
-#endif
-#if REM_PREF
-        uint32_t nent[REM_MU];  // next iteration's list entries, loaded one iteration ahead
-#pragma unroll
-        for (int u = 0; u < REM_MU; ++u) {
-            const uint32_t i = wbase + u * 32 + lane;
-            nent[u] = i < mend ? __ldcg(ML + i) : 0u;
-        }
-#endif
         for (uint32_t i0 = wbase; i0 < mend; i0 += wstride) {
             uint32_t ent[REM_MU], rw[REM_MU], x[REM_MU];
             bool live[REM_MU];
@@ -1279,27 +1258,7 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
             for (int u = 0; u < REM_MU; ++u) {
                 const uint32_t i = i0 + u * 32 + lane;
                 live[u] = i < mend;
-#if REM_PREF
-                ent[u] = nent[u];
-                const uint32_t j = i + wstride;
-                nent[u] = j < mend ? __ldcg(ML + j) : 0u;
-#if REM_PREF > 1
-                if (j < mend) {  // warm L2 with the next member's rows (no registers held)
-                    const uint32_t cn = nent[u] & ~CARRY;
-                    const real_t *b = Pc + cn;
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(b));
-                    asm volatile("prefetch.global.L2 [%0];" ::"l"(p.dd + cn));
-                    if (cn >= nx) asm volatile("prefetch.global.L2 [%0];" ::"l"(b - nx));
-                    if (cn + nx < p.ncells) asm volatile("prefetch.global.L2 [%0];" ::"l"(b + nx));
-                    if (DIM == 3) {
-                        if (cn >= p.plane32) asm volatile("prefetch.global.L2 [%0];" ::"l"(b - p.plane32));
-                        if (cn + p.plane32 < p.ncells) asm volatile("prefetch.global.L2 [%0];" ::"l"(b + p.plane32));
-                    }
-                }
-#endif
-#else
                 ent[u] = live[u] ? __ldcg(ML + i) : 0u;
-#endif
             }
 #pragma unroll
             for (int u = 0; u < REM_MU; ++u) {
