@@ -109,6 +109,7 @@ struct Ctl {
     unsigned fc[3];                 // FIM: check-list length per rotating slot
 #ifdef EIK_DIAG
     unsigned long long dg[4][26];   // remedy rounds by log2|R_r|: count, phase B ns, phase A ns, members
+    unsigned long long du[3][26];   // update iterations by log2|A_k|: count, ns, cells
 #endif
 };
 
@@ -970,6 +971,19 @@ __device__ __forceinline__ void update_body(const KP &p)
         }
         if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
         const unsigned long long m = ranks_len<MR>(p, (int)((it + 1) % 3));
+#ifdef EIK_DIAG
+        if (lead) {
+            unsigned long long tnow;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tnow));
+            const int bk = n ? min(25, 31 - __clz(n)) : 0;
+            if (it > p.it0) {
+                ctl->du[0][bk] += 1;
+                ctl->du[1][bk] += tnow - ctl->du[2][25];
+                ctl->du[2][bk] += n;
+            }
+            ctl->du[2][25] = tnow;  // last barrier time (bucket 25 of cells is never reached)
+        }
+#endif
         if (p.slab) continue;  // the host reduces the counts and decides
         if (lead) {
             ctl->iters = it + 1;
@@ -993,8 +1007,11 @@ __device__ __forceinline__ void update_body(const KP &p)
     }
 }
 
+#ifndef UPD_MINB
+#define UPD_MINB 3  // update step: CTAs per SM the register budget is sized for
+#endif
 template <int DIM, int SOL>
-__global__ void __launch_bounds__(BLOCK, 3) k_update(KP p)
+__global__ void __launch_bounds__(BLOCK, UPD_MINB) k_update(KP p)
 {
     update_body<DIM, SOL, false>(p);
 }
@@ -2324,6 +2341,10 @@ int EIK_FN(eik_ifim_solve)(const eik_geom *g, real_t *phi, const real_t *speed, 
         fprintf(stderr, "[eik diag] remedy member words %llu sectors %llu calls %llu\n",
                 (unsigned long long)c[1].nz_words, (unsigned long long)c[1].nz_sectors,
                 (unsigned long long)c[1].sum);
+        for (int k = 0; k < 25; ++k)
+            if (c[0].du[0][k])
+                fprintf(stderr, "[eik diag] update |A|~2^%2d iterations %6llu cells %12llu  %9.3f ms  (%.2f us per iteration)\n",
+                        k, c[0].du[0][k], c[0].du[2][k], c[0].du[1][k] * 1e-6, c[0].du[1][k] * 1e-3 / c[0].du[0][k]);
         for (int k = 0; k < 26; ++k)
             if (c[1].dg[0][k])
                 fprintf(stderr, "[eik diag] |R|~2^%2d rounds %6llu members %12llu  B %9.3f ms  A %9.3f ms  (%.2f/%.2f us per round)\n",
