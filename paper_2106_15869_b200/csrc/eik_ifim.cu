@@ -378,8 +378,10 @@ __device__ __forceinline__ bool grid_barrier_n(Ctl *ctl, unsigned nblocks, const
     if (threadIdx.x == 0) {
         volatile unsigned *vgen = &ctl->bar_gen;
         const unsigned gen = *vgen;
-        if (p && p->mr) __threadfence_system();
-        else __threadfence();
+        // gpu-scope release is enough here even across ranks: the last arriver
+        // acquires every CTA's arrival, then publishes system-wide (fence.sc.sys
+        // before the cross-rank atomic), and causality order is transitive
+        __threadfence();
         const unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
         unsigned ok = 1;
         if (arrived == nblocks - 1) {
@@ -1019,9 +1021,17 @@ __global__ void __launch_bounds__(BLOCK, UPD_MINB) k_update(KP p)
 // Multi-rank: rank groups of one launch (emulation on one GPU, kps[] in device
 // memory) or one rank per GPU (kps[0]); peers through device-visible pointers.
 template <int DIM, int SOL>
-__global__ void __launch_bounds__(BLOCK, 3) k_update_mr(const KP *__restrict__ kps, uint32_t per_group)
+__global__ void __launch_bounds__(BLOCK, UPD_MINB) k_update_mr(const KP *__restrict__ kps, uint32_t per_group)
 {
     update_body<DIM, SOL, true>(kps[blockIdx.x / per_group]);
+}
+
+// One rank per launch (one process per GPU): the rank's parameters stay in the
+// kernel parameter space instead of being read through a pointer.
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK, UPD_MINB) k_update_mr1(KP p)
+{
+    update_body<DIM, SOL, true>(p);
 }
 
 // ---------------------------------------------------------------------------
@@ -1370,6 +1380,12 @@ template <int DIM, int SOL>
 __global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy_mr(const KP *__restrict__ kps, uint32_t per_group)
 {
     remedy_body<DIM, SOL, true>(kps[blockIdx.x / per_group], nullptr);
+}
+
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy_mr1(KP p)
+{
+    remedy_body<DIM, SOL, true>(p, nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -2643,9 +2659,16 @@ int eik_mr_run(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_be
     }
     CK(cudaMemcpyAsync(kps_dev, host.data(), sizeof(KP) * nl, cudaMemcpyHostToDevice, st));
     int pgo = 0;
-    int rc = Engine<3, SOL_U3>::update_mr(kps_dev, nl, st, pgo);
+    int rc;
+    if (nl == 1) {  // one rank on this device: parameters by value
+        host[0].gb0 = 0;
+        host[0].gnb = 0;
+        rc = coop_launch(k_update_mr1<3, SOL_U3>, host[0], nullptr, false, st, "EIK_UPD_BLOCKS_PER_SM", 0);
+    } else {
+        rc = Engine<3, SOL_U3>::update_mr(kps_dev, nl, st, pgo);
+        if (!rc && (uint32_t)pgo != pg) return fail(EIK_ECUDA, "group size mismatch");
+    }
     if (rc) return rc;
-    if ((uint32_t)pgo != pg) return fail(EIK_ECUDA, "group size mismatch");
     ev.rec(1, st);
     // build: per local rank (reads the neighbours' final phi; the update's last world barrier ordered it)
     for (int i = 0; i < nl; ++i) {
@@ -2663,7 +2686,13 @@ int eik_mr_run(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_be
     }
     KP *kps_dev_r = kps_dev + EIK_MAX_RANKS;
     CK(cudaMemcpyAsync(kps_dev_r, host.data(), sizeof(KP) * nl, cudaMemcpyHostToDevice, st));
-    rc = Engine<3, SOL_U3>::remedy_mr(kps_dev_r, nl, st, pgo);
+    if (nl == 1) {
+        host[0].gb0 = 0;
+        host[0].gnb = 0;
+        rc = coop_launch(k_remedy_mr1<3, SOL_U3>, host[0], nullptr, false, st, "EIK_REM_BLOCKS_PER_SM", 0);
+    } else {
+        rc = Engine<3, SOL_U3>::remedy_mr(kps_dev_r, nl, st, pgo);
+    }
     if (rc) return rc;
     ev.rec(3, st);
     // global stats live in rank 0's control blocks; errors in any local rank's
