@@ -115,7 +115,8 @@ def make_workload(torch, dev, config, n):
                         workload_desc(config, n))
     blk = max(1, n // 16)
     kk = torch.arange(n, device=dev) // blk
-    F = torch.where(((kk[:, None, None] + kk[None, :, None] + kk[None, None, :]) % 2) == 0, 1.0, 0.01).double()
+    one, slow = torch.tensor(1.0, dtype=torch.float64), torch.tensor(0.01, dtype=torch.float64)  # exact 1:100
+    F = torch.where(((kk[:, None, None] + kk[None, :, None] + kk[None, None, :]) % 2) == 0, one, slow)
     c = n // 2
     return Workload("cfg4", n, 1.0, F, [(c, c, c)], workload_desc(config, n))
 

@@ -457,18 +457,28 @@ __device__ __forceinline__ bool palette_on(const KP &p) { return p.pstate && __l
 // tiles (3D) or 16-row tiles (2D), so a CTA's consecutive members cover their
 // own y +- 1 / z +- 1 neighbour rows (L1 reuse).  Positions beyond the grid
 // (tile padding) map to an out-of-range word.
+#ifndef TILE_LY
+#define TILE_LY 2  // log2 rows per tile in y (3D)
+#endif
+#ifndef TILE_LZ
+#define TILE_LZ 2  // log2 rows per tile in z (3D)
+#endif
+#ifndef TILE_L2D
+#define TILE_L2D 4  // log2 rows per tile (2D)
+#endif
 template <int DIM>
 __device__ __forceinline__ uint32_t word_at(const KP &p, uint32_t l)
 {
-    const uint32_t in = l & 15u, t = l >> 4;
+    constexpr uint32_t LT = DIM == 3 ? TILE_LY + TILE_LZ : TILE_L2D;
+    const uint32_t in = l & ((1u << LT) - 1u), t = l >> LT;
     const uint32_t tile = fdiv(t, p.fW), wx = t - tile * p.W;
     uint32_t y, z;
     if (DIM == 3) {
         const uint32_t tz = fdiv(tile, p.fnty4), ty = tile - tz * p.nty4;
-        y = ty * 4 + (in & 3u);
-        z = tz * 4 + (in >> 2);
+        y = (ty << TILE_LY) + (in & ((1u << TILE_LY) - 1u));
+        z = (tz << TILE_LZ) + (in >> TILE_LY);
     } else {
-        y = tile * 16 + in;
+        y = (tile << TILE_L2D) + in;
         z = 0;
     }
     if (y >= (uint32_t)p.ny || z >= (uint32_t)p.nz) return 0xffffffffu;
@@ -1804,13 +1814,13 @@ int make_layout(const eik_geom *g, Layout &L)
     L.off_kps = o; o += al(2 * EIK_MAX_RANKS * sizeof(KP));
     // member-list traversal (word_at): 3D groups of 4x4 rows, 2D groups of 16 rows, per x-word
     if (g->ndim == 3) {
-        L.nty4 = (uint32_t)((g->ny + 3) / 4);
-        L.ntt = (uint32_t)((g->nz + 3) / 4);
-        L.npos = L.nty4 * L.ntt * 16 * L.W;
+        L.nty4 = (uint32_t)((g->ny + (1 << TILE_LY) - 1) >> TILE_LY);
+        L.ntt = (uint32_t)((g->nz + (1 << TILE_LZ) - 1) >> TILE_LZ);
+        L.npos = (L.nty4 * L.ntt << (TILE_LY + TILE_LZ)) * L.W;
     } else {
         L.nty4 = 0;
-        L.ntt = (uint32_t)((g->ny + 15) / 16);
-        L.npos = L.ntt * 16 * L.W;
+        L.ntt = (uint32_t)((g->ny + (1 << TILE_L2D) - 1) >> TILE_L2D);
+        L.npos = (L.ntt << TILE_L2D) * L.W;
     }
     L.total = o;
     return EIK_OK;

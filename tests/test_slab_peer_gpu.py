@@ -53,7 +53,7 @@ def test_peer_slabs_bit_identical(R, kind):
 def test_peer_slabs_512_matches_single():
     n = 256
     k = torch.arange(n, device="cuda") // (n // 16)
-    F = torch.where(((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2) == 0, 1.0, 0.01).double()
+    F = torch.where(((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2) == 0, torch.tensor(1.0, dtype=torch.float64), torch.tensor(0.01, dtype=torch.float64))
     state = torch.zeros((n, n, n), dtype=torch.uint8, device="cuda")
     c = n // 2
     g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), np.inf, dtype=torch.float64, device="cuda"),

@@ -16,7 +16,7 @@ import torch, paper_2106_15869_b200 as eik
 n = int(sys.argv[3]); kind = sys.argv[4]
 k = torch.arange(n, device="cuda") // max(1, n // 16)
 if kind == "checker":
-    F = torch.where(((k[None, None, :] + k[None, :, None] + k[:, None, None]) % 2) == 0, 1.0, 0.01).double()
+    F = torch.where(((k[None, None, :] + k[None, :, None] + k[:, None, None]) % 2) == 0, torch.tensor(1.0, dtype=torch.float64), torch.tensor(0.01, dtype=torch.float64))
     seeds = [(n // 2, n // 2, n // 2)]
 else:
     import numpy as np

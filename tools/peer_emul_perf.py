@@ -12,7 +12,7 @@ from paper_2106_15869_b200.slab_peer import EmulatedSlabs  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 k = torch.arange(n, device="cuda") // (n // 16)
-F = torch.where(((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2) == 0, 1.0, 0.01).double()
+F = torch.where(((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2) == 0, torch.tensor(1.0, dtype=torch.float64), torch.tensor(0.01, dtype=torch.float64))
 st0 = torch.zeros((n, n, n), dtype=torch.uint8, device="cuda")
 c = n // 2
 g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), float("inf"), dtype=torch.float64, device="cuda"),

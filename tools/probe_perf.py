@@ -6,7 +6,7 @@ import paper_2106_15869_b200 as eik
 
 def checker(n, blk):
     k = torch.arange(n, device="cuda") // blk
-    return torch.where(((k[None, None, :] + k[None, :, None] + k[:, None, None]) % 2) == 0, 1.0, 0.01).double()
+    return torch.where(((k[None, None, :] + k[None, :, None] + k[:, None, None]) % 2) == 0, torch.tensor(1.0, dtype=torch.float64), torch.tensor(0.01, dtype=torch.float64))
 
 def run(name, n, F, seeds, reps=2):
     dev = torch.device("cuda:0")
