@@ -13,9 +13,15 @@ sys.path.insert(0, sys.argv[1])
 from paper_2106_15869_b200 import _native
 _native.LIB = os.path.join(os.path.dirname(_native.LIB), sys.argv[2])
 import torch, paper_2106_15869_b200 as eik
-n = int(sys.argv[3]); kind = sys.argv[4]
+n = int(sys.argv[3]); kind = sys.argv[4]; h = 1.0
 k = torch.arange(n, device="cuda") // max(1, n // 16)
-if kind == "checker":
+if kind == "cfg5":
+    sys.path.insert(0, sys.argv[1])
+    import bench
+    w = bench.make_workload(torch, torch.device("cuda"), "cfg5", n)
+    F, seeds = w.F, w.seeds
+    h = w.h
+elif kind == "checker":
     F = torch.where(((k[None, None, :] + k[None, :, None] + k[:, None, None]) % 2) == 0, torch.tensor(1.0, dtype=torch.float64), torch.tensor(0.01, dtype=torch.float64))
     seeds = [(n // 2, n // 2, n // 2)]
 else:
@@ -25,7 +31,7 @@ else:
     seeds = [tuple(int(v) for v in rng.integers(0, n, 3)) for _ in range(16)]
 best = None
 for r in range(3):
-    g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), float("inf"), dtype=torch.float64, device="cuda"),
+    g = eik.Grid3D(n, n, n, h, (0.0, 0.0, 0.0), torch.full((n, n, n), float("inf"), dtype=torch.float64, device="cuda"),
                    F, torch.zeros((n, n, n), dtype=torch.uint8, device="cuda"))
     res = eik.solve_ifim(g, eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in seeds)))
     d = res.stats.device_ms
