@@ -105,3 +105,28 @@ def test_exact_distance_error_equals_oracle_64():
     e_gpu, e_cpu = np.abs(res.phi - exact), np.abs(ref.phi - exact)
     assert np.max(np.abs(e_gpu - e_cpu)) <= 1e-10
     assert e_gpu.max() <= 0.6 * np.log(n)
+
+
+@pytest.mark.slow
+def test_cfg5_full_size_ifim_equals_fixpoint():
+    """cfg5 at its full 1024^3 (BASELINE.json configs[4] on one GPU): the iFIM field equals the
+    GPU fixpoint ground truth (E/oracle.py) within 1e-9 (the reference's method-vs-fixpoint
+    gate, T/test_fim.py:23 / T/test_ifim.py:30; measured 2.2e-10) and satisfies the equation."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+
+    n = 1024
+    dev = torch.device("cuda:0")
+    w = bench.make_workload(torch, dev, "cfg5", n)
+    bc = eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in w.seeds))
+    g = eik.Grid3D(n, n, n, w.h, (0.0, 0.0, 0.0), torch.full((n, n, n), np.inf, dtype=torch.float64, device=dev),
+                   w.F, torch.zeros((n, n, n), dtype=torch.uint8, device=dev))
+    a = eik.solve_ifim(g, bc).phi
+    assert eik.max_residual(g) <= 1e-9
+    g.phi.fill_(np.inf)
+    g.state.zero_()
+    b = eik.solve_fixpoint(g, bc).phi
+    assert eik.field_max_diff(a, b) <= 1e-9

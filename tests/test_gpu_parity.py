@@ -293,3 +293,49 @@ def test_host_grid_large_result_copy_is_independent():
     res = eik.solve_ifim(gn, eik.seed_point(gn, (80, 80, 80), 0.0))
     assert isinstance(res.phi, np.ndarray) and np.array_equal(res.phi, gn.phi) and not np.shares_memory(res.phi, gn.phi)
     assert np.array_equal(res.phi, ref.phi.cpu().numpy())
+
+
+def _cfg2(n):
+    """BASELINE.json configs[1]: 2D n^2 on [0,1]^2, F = 1 + 0.5 sin(2 pi x) sin(2 pi y)
+    at the cell centres, 8 distinct random point seeds (rng 2106)."""
+    h = 1 / (n - 1)
+    x = h * np.arange(n)
+    xx, yy = np.meshgrid(x, x)
+    F = 1 + 0.5 * np.sin(2 * np.pi * xx) * np.sin(2 * np.pi * yy)
+    rng = np.random.default_rng(2106)
+    cells = []
+    while len(cells) < 8:
+        c = tuple(int(v) for v in rng.integers(0, n, 2))
+        if c not in cells:
+            cells.append(c)
+    return h, F, cells
+
+
+@pytest.mark.slow
+def test_cfg2_1024_bit_exact_vs_oracle():
+    n = 1024
+    h, F, cells = _cfg2(n)
+    g = eik.new_grid(n, n, h, h, speed=F)
+    res = eik.solve_ifim(g, eik.BoundaryCondition(tuple((eik.CellIndex(i, j), 0.0) for i, j in cells)))
+    ref = cpu.solve_ifim((n, n), (h, h), F, [j * n + i for i, j in cells], [0.0] * len(cells), threads=16)
+    assert np.array_equal(res.phi.view(np.uint64), ref.phi.view(np.uint64))
+    assert (res.stats.solver_calls, res.stats.iterations, res.stats.peak_remedy) == (
+        ref.stats["solver_calls"], ref.stats["iterations"], ref.stats["peak_remedy"])
+    assert res.stats.active_history == ref.active_history
+
+
+@pytest.mark.slow
+def test_cfg2_full_size_properties():
+    """cfg2 at its full 4096^2: iFIM reaches the GPU fixpoint field and satisfies the equation."""
+    n = 4096
+    h, F, cells = _cfg2(n)
+    dev = torch.device("cuda:0")
+    mk = lambda: eik.Grid(n, n, h, h, (0.0, 0.0), torch.full((n, n), np.inf, dtype=torch.float64, device=dev),
+                          torch.as_tensor(F, device=dev), torch.zeros((n, n), dtype=torch.uint8, device=dev))
+    bc = eik.BoundaryCondition(tuple((eik.CellIndex(i, j), 0.0) for i, j in cells))
+    g1, g2 = mk(), mk()
+    a = eik.solve_ifim(g1, bc)
+    b = eik.solve_fixpoint(g2, bc)
+    assert eik.field_max_diff(a.phi, b.phi) <= 1e-9
+    assert eik.max_residual(g1) <= 1e-9
+    assert a.stats.peak_remedy > 0 and a.stats.solver_calls > n * n
