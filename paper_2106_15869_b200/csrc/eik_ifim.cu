@@ -73,7 +73,7 @@ constexpr real_t kSqrt2 = (real_t)1.4142135623730951;
 constexpr real_t DISC_CLAMP = (real_t)1e-12;
 constexpr real_t R_HALF = (real_t)0.5, R_ONE = (real_t)1.0, R_TWO = (real_t)2.0, R_THREE = (real_t)3.0, R_ZERO = (real_t)0.0;
 
-// IEEE bits of a non-negative value, ordered like the value (atomicMax reductions, palette keys)
+// IEEE bits of a non-negative value, ordered like the value (atomicMax reductions)
 #if EIK_SINGLE
 __device__ __forceinline__ unsigned long long bits_of(float x) { return (unsigned long long)__float_as_uint(x); }
 #else
@@ -163,12 +163,7 @@ struct KP {
     real_t *P0, *P1;         // P0 = caller phi, P1 = workspace copy
     const real_t *F;         // speed
     real_t *dd;              // delta / F (uniform solvers)
-    // speed palette (piecewise-constant F): 1-byte index per cell + exact coefficient table
-    uint8_t *pidx;
-    real_t *ptab;            // [PAL_MAX] delta/F_k (uniform) or F_k (anisotropic)
-    unsigned long long *phash;  // [PAL_SLOTS] F bit patterns (open addressing)
-    uint32_t *pslot;         // [PAL_SLOTS] slot -> palette index
-    uint32_t *pstate;        // [0] distinct count, [1] overflow, [2] palette in use
+    uint8_t *lab;            // FIM labels (one byte per cell)
     const uint8_t *state;
     uint32_t *Bt;                 // touched bitmap (update step labels: not FAR)
     uint32_t *L0, *L1;            // update-step cell worklists
@@ -437,21 +432,12 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, un
     return t;
 }
 
-constexpr int PAL_MAX = 255;     // palette entries (uint8 index)
-constexpr int PAL_SLOTS = 1024;  // hash slots
-constexpr unsigned long long PAL_EMPTY = ~0ull;
-
-// Per-cell coefficient of the local solver: d = delta/F (uniform) or F
-// (anisotropic), from the palette when the speed field has <= 255 distinct
-// values (same IEEE value, 1 byte of traffic instead of 8), else from the array.
+// Per-cell coefficient of the local solver: d = delta/F (uniform) or F (anisotropic).
 template <int SOL>
-__device__ __forceinline__ real_t coef(const KP &p, bool pal, uint32_t c)
+__device__ __forceinline__ real_t coef(const KP &p, uint32_t c)
 {
-    if (pal) return __ldg(p.ptab + __ldg(p.pidx + c));
     return (SOL == SOL_A2) ? __ldg(p.F + c) : __ldg(p.dd + c);
 }
-
-__device__ __forceinline__ bool palette_on(const KP &p) { return p.pstate && __ldg(p.pstate + 2) != 0; }
 
 // Traversal order of the remedy member list: x-word columns of 4x4 (y, z) row
 // tiles (3D) or 16-row tiles (2D), so a CTA's consecutive members cover their
@@ -546,7 +532,7 @@ __device__ __forceinline__ void gather_issue(const KP &p, const real_t *__restri
             else if (p.mr && p.hi.valid)
                 s.u = ldcg((Pc == p.P0 ? p.hi.P0 : p.hi.P1) + (q.y * p.nx32 + q.x0 + lane));
         }
-        s.k = coef<SOL>(p, palette_on(p), c);
+        s.k = coef<SOL>(p, c);
     }
 }
 
@@ -633,71 +619,6 @@ __global__ void k_seed(real_t *phi, uint8_t *state, const int64_t *idx, const do
     }
 }
 
-// ---- speed palette ---------------------------------------------------------
-__device__ __forceinline__ uint32_t pal_hash(unsigned long long k)
-{
-    k ^= k >> 33;
-    k *= 0xff51afd7ed558ccdull;
-    k ^= k >> 33;
-    return (uint32_t)k & (PAL_SLOTS - 1);
-}
-
-// Insert the distinct F bit patterns into an open-addressing table (warp-deduplicated).
-__global__ void k_palette_insert(KP p, int64_t n)
-{
-    const unsigned lane = lane_id();
-    for (int64_t i0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; i0 < n; i0 += (int64_t)gridDim.x * blockDim.x) {
-        if (*(volatile uint32_t *)(p.pstate + 1)) return;  // overflow: give up
-        const int64_t i = i0 + lane;
-        const bool in = i < n;
-        const unsigned long long key = in ? bits_of(p.F[i]) : PAL_EMPTY;
-        const unsigned grp = __match_any_sync(FULL, key);
-        if (!in || lane != (unsigned)(__ffs(grp) - 1)) continue;
-        uint32_t h = pal_hash(key);
-        for (int probe = 0;; ++probe) {
-            if (probe == PAL_SLOTS) {
-                atomicExch(p.pstate + 1, 1u);
-                break;
-            }
-            const unsigned long long old = atomicCAS(p.phash + h, PAL_EMPTY, key);
-            if (old == PAL_EMPTY) {
-                if (atomicAdd(p.pstate, 1u) >= (unsigned)PAL_MAX) atomicExch(p.pstate + 1, 1u);
-                break;
-            }
-            if (old == key) break;
-            h = (h + 1) & (PAL_SLOTS - 1);
-        }
-    }
-}
-
-// Compact the occupied slots into palette indices; table = the solver coefficient
-// computed with the same IEEE operation as the per-cell array (delta / F).
-template <bool UNIFORM>
-__global__ void k_palette_finalize(KP p)
-{
-    __shared__ uint32_t cnt;
-    if (threadIdx.x == 0) cnt = 0;
-    __syncthreads();
-    const bool ok = p.pstate[1] == 0;
-    for (uint32_t s = threadIdx.x; s < (uint32_t)PAL_SLOTS; s += blockDim.x) {
-        const unsigned long long key = p.phash[s];
-        if (!ok || key == PAL_EMPTY) continue;
-        const uint32_t k = atomicAdd(&cnt, 1u);
-        p.pslot[s] = k;
-        const real_t f = real_of_bits(key);
-        p.ptab[k] = UNIFORM ? p.delta / f : f;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) p.pstate[2] = ok ? 1u : 0u;
-}
-
-__device__ __forceinline__ uint8_t pal_index(const KP &p, real_t f)
-{
-    const unsigned long long key = bits_of(f);
-    uint32_t h = pal_hash(key);
-    while (__ldg(p.phash + h) != key) h = (h + 1) & (PAL_SLOTS - 1);
-    return (uint8_t)__ldg(p.pslot + h);
-}
 
 // One pass over all words: copy phi into the second buffer, d = delta / F,
 // touched = blocked, fixed = blocked | source, optionally clear set bitmaps.
@@ -707,7 +628,6 @@ __global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_
     const unsigned lane = lane_id();
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
-    const bool pal = palette_on(p);
     for (uint32_t w = gw; w < p.nwords; w += GW) {
         const WPos q = wpos<DIM>(p, w);
         const bool in = (q.rowm >> lane) & 1u;
@@ -716,8 +636,7 @@ __global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_
         if (in) {
             st = p.state[c];
             if (copy_phi) p.P1[c] = p.P0[c];
-            if (pal) p.pidx[c] = pal_index(p, p.F[c]);
-            else if (UNIFORM) p.dd[c] = p.delta / p.F[c];
+            if (UNIFORM) p.dd[c] = p.delta / p.F[c];
         }
         const uint32_t blk = __ballot_sync(FULL, in && st == ST_BLOCKED);
         const uint32_t src = __ballot_sync(FULL, in && st == ST_SOURCE);
@@ -857,7 +776,6 @@ __device__ __forceinline__ void update_body(const KP &p)
         }
     }
     const uint32_t nx = (uint32_t)p.nx, ny = (uint32_t)p.ny, nz = (uint32_t)p.nz;
-    const bool pal = palette_on(p);
     for (int64_t it = p.it0; it < p.it0 + p.max_it; ++it) {
         const int par = (int)(it & 1);
         const real_t *__restrict__ Pc = par ? p.P1 : p.P0;
@@ -907,7 +825,7 @@ __device__ __forceinline__ void update_body(const KP &p)
                         else if (MR && p.hi.valid)  // neighbour rank's bottom plane
                             t.u = __ldcg((par ? p.hi.P1 : p.hi.P0) + (y[u] * nx + x[u]));
                     }
-                    t.k = coef<SOL>(p, pal, cc);
+                    t.k = coef<SOL>(p, cc);
                 }
             }
 #pragma unroll
@@ -1245,7 +1163,6 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
     }
     const uint32_t nx = p.nx32, ny = (uint32_t)p.ny, nz = (uint32_t)p.nz;
     uint32_t *ML = p.L0;
-    const bool pal = palette_on(p);
     for (int64_t rr = p.it0; rr < p.it0 + p.max_it; ++rr) {
         const uint32_t r = (uint32_t)rr;
 #ifdef EIK_DIAG
@@ -1326,7 +1243,7 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
                         else if (MR && p.hi.valid)
                             t.u = __ldcg((par ? p.hi.P1 : p.hi.P0) + (y * nx + x[u]));
                     }
-                    t.k = coef<SOL>(p, pal, c);
+                    t.k = coef<SOL>(p, c);
                 }
             }
 #pragma unroll
@@ -1480,7 +1397,7 @@ __global__ void __launch_bounds__(BLOCK) k_fixpoint(KP p)
 //      once per distinct cell (:110-124)
 //   4  values of the distinct checks from the post-phase-2 field
 //   5  a check that drops by more than tol is written and re-activated (:126-138)
-// Labels live in the palette-index buffer (unused by FIM), the claim bitmap in
+// Labels live in their own byte buffer, the claim bitmap in
 // the R0 slot; both are cleared by the host before the launch.
 // ---------------------------------------------------------------------------
 constexpr uint8_t FIM_ACTIVE = 1, FIM_SETTLED = 2;  // E/fim.py:29 (FAR = 0)
@@ -1500,7 +1417,7 @@ __device__ __forceinline__ real_t cell_solve(const KP &p, const real_t *P, uint3
         t.d = z > 0 ? __ldcg(P + c - p.plane32) : INFINITY;
         t.u = z + 1 < (uint32_t)p.nz ? __ldcg(P + c + p.plane32) : INFINITY;
     }
-    t.k = coef<SOL>(p, false, c);
+    t.k = coef<SOL>(p, c);
     return solve<DIM, SOL>(p, t);
 }
 
@@ -1526,7 +1443,7 @@ __global__ void __launch_bounds__(BLOCK) k_fim(KP p)
     Ctl *ctl = p.ctl;
     real_t *P = p.P0;
     real_t *V = p.P1;       // values per list slot (phases 1 and 4)
-    uint8_t *lab = p.pidx;  // FIM labels
+    uint8_t *lab = p.lab;  // FIM labels
     uint32_t *claim = p.R0b;
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nthr = gridDim.x * blockDim.x;
     const uint32_t bstride = gridDim.x * BLOCK;
@@ -1763,7 +1680,7 @@ struct Layout {
     int64_t N;
     uint32_t W, nwords, npos, nty4, ntt;
     size_t off_phi2, off_dd, off_bt, off_l0, off_l1, off_l2;
-    size_t off_r0, off_d0, off_d1, off_f, off_pidx, off_ptab, off_phash, off_pslot, off_pstate;
+    size_t off_r0, off_d0, off_d1, off_f, off_lab;
     size_t off_hist, off_ctl_u, off_ctl_r, off_kps, total;
     int64_t cap_upd, cap_rem;
 };
@@ -1803,11 +1720,7 @@ int make_layout(const eik_geom *g, Layout &L)
     L.off_d0 = o; o += al(bm);
     L.off_d1 = o; o += al(bm);
     L.off_f = o; o += al(bm);
-    L.off_pidx = o; o += al((size_t)L.N);
-    L.off_ptab = o; o += al(PAL_MAX * sizeof(real_t) + 8);
-    L.off_phash = o; o += al(PAL_SLOTS * 8);
-    L.off_pslot = o; o += al(PAL_SLOTS * 4);
-    L.off_pstate = o; o += al(16);
+    L.off_lab = o; o += al((size_t)L.N);  // FIM labels
     L.off_hist = o; o += al((size_t)(L.cap_upd + 2) * 8);
     L.off_ctl_u = o; o += al(sizeof(Ctl));
     L.off_ctl_r = o; o += al(sizeof(Ctl));
@@ -1870,11 +1783,7 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, real_t *phi, const real
     p.D0b = (uint32_t *)(b + L.off_d0);
     p.D1b = (uint32_t *)(b + L.off_d1);
     p.Fb = (uint32_t *)(b + L.off_f);
-    p.pidx = (uint8_t *)(b + L.off_pidx);
-    p.ptab = (real_t *)(b + L.off_ptab);
-    p.phash = (unsigned long long *)(b + L.off_phash);
-    p.pslot = (uint32_t *)(b + L.off_pslot);
-    p.pstate = (uint32_t *)(b + L.off_pstate);
+    p.lab = (uint8_t *)(b + L.off_lab);
     return p;
 }
 
@@ -1945,16 +1854,6 @@ struct Engine {
     // phi copy (optional), d = delta/F, touched (optional) and the fixed brick bitmap
     static int prep(KP &p, bool copy_phi, bool touched, cudaStream_t st)
     {
-        CK(cudaMemsetAsync(p.pstate, 0, 16, st));
-        if (getenv("EIK_PALETTE")) {  // opt-in: measured slower on the 512^3 checkerboard (latency-bound gathers)
-            CK(cudaMemsetAsync(p.phash, 0xff, PAL_SLOTS * sizeof(unsigned long long), st));
-            const int64_t N = p.nx * p.ny * p.nz;
-            k_palette_insert<<<(int)std::min<int64_t>((N + 255) / 256, (int64_t)num_sms() * 8), 256, 0, st>>>(p, N);
-            CK(cudaGetLastError());
-            if (SOL == SOL_A2) k_palette_finalize<false><<<1, 256, 0, st>>>(p);
-            else k_palette_finalize<true><<<1, 256, 0, st>>>(p);
-            CK(cudaGetLastError());
-        }
         const int grid = stream_grid(p.nwords);
         if (SOL == SOL_A2) k_prep<DIM, false><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched);
         else k_prep<DIM, true><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched);
@@ -2464,7 +2363,7 @@ int EIK_FN(eik_solve_fim)(const eik_geom *g, real_t *phi, const real_t *speed, u
     rc = dispatch(g, [&](auto E) {
         int r = E.prep(p, false, true, st);
         if (r) return r;
-        CK(cudaMemsetAsync(p.pidx, 0, (size_t)L.N, st));          // labels: FAR (after prep: palette slot)
+        CK(cudaMemsetAsync(p.lab, 0, (size_t)L.N, st));           // labels: FAR
         CK(cudaMemsetAsync(p.R0b, 0, (size_t)L.nwords * 4, st));  // claims
         r = E.init_active(p, seed_idx, nseeds, st);
         if (r) return r;
