@@ -64,5 +64,5 @@ for p in range(2):
 for v, rs in res.items():
     if rs:
         b = min(rs, key=lambda d: d["total"])
-        print(f"{v:40s} total {b['total']:8.2f} update {b['update']:7.2f} remedy {b['remedy']:8.2f}  "
+        print(f"{v:40s} total {b['total']:8.2f} update {b['update']:7.2f} build {b['build']:6.3f} remedy {b['remedy']:8.2f}  "
               f"(all totals {[round(d['total'], 1) for d in rs]}) calls {b['calls']}")
