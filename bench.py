@@ -352,6 +352,33 @@ def peer_slabs_possible(torch, dev, world, local):
     return bool(t.item())
 
 
+def peer_slabs_verify(torch, dev, world, rank):
+    """Small multi-rank solve through DistributedSlabs compared bit for bit (phi, stats) with a
+    single-device solve of the same problem on this rank: guards the cross-GPU memory ordering
+    before the timed run trusts it."""
+    import paper_2106_15869_b200 as eik
+    from paper_2106_15869_b200.slab import SlabPartition
+    from paper_2106_15869_b200.slab_peer import DistributedSlabs
+
+    n = max(32, 8 * world)
+    k = torch.arange(n, device=dev) // 4
+    F = torch.where(((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2) == 0,
+                    torch.tensor(1.0, dtype=torch.float64), torch.tensor(0.02, dtype=torch.float64))
+    seeds = [(3, 5, 2), (n - 4, n // 2, n - 3)]
+    g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), float("inf"), dtype=torch.float64,
+                                                             device=dev),
+                   F, torch.zeros((n, n, n), dtype=torch.uint8, device=dev))
+    ref = eik.solve_ifim(g, eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in seeds)))
+    z0, z1 = SlabPartition(n, world).bounds(rank)
+    ds = DistributedSlabs((n, n, n), 1.0)
+    st = torch.zeros((z1 - z0, n, n), dtype=torch.uint8, device=dev)
+    phi, s = ds.solve(F[z0:z1].contiguous(), st, [((kk * n + j) * n + i, 0.0) for i, j, kk in seeds])
+    same = torch.equal(phi, ref.phi[z0:z1]) and s.solver_calls == ref.stats.solver_calls and \
+        s.active_history == ref.stats.active_history
+    del ds
+    return same
+
+
 def make_peer_step(torch, dev, w, world, rank):
     """This rank's share of ONE z-sharded solve in the fused peer-memory kernels
     (paper_2106_15869_b200/slab_peer.py): neighbour planes read over NVLink inside the
@@ -404,10 +431,14 @@ def run_ours(args):
     if world > 1 and not args.host_slabs and peer_slabs_possible(torch, dev, world, local):
         import torch.distributed as dist
 
-        try:  # symmetric-memory slabs + one probe solve; any rank failing sends every rank to the NCCL path
+        try:  # symmetric-memory slabs, a verified small solve and one probe solve; any rank failing
+            # sends every rank to the NCCL path
+            ok = int(peer_slabs_verify(torch, dev, world, rank))
+            if not ok:
+                print(f"[bench] peer-memory slabs disagree with the single-device solve on rank {rank}",
+                      file=sys.stderr, flush=True)
             step, mode = make_peer_step(torch, dev, w, world, rank), "peer"
             step()
-            ok = 1
         except Exception as e:  # noqa: BLE001
             print(f"[bench] peer-memory slabs unavailable on rank {rank}: {e!r}", file=sys.stderr, flush=True)
             ok = 0
