@@ -405,6 +405,46 @@ def make_peer_step(torch, dev, w, world, rank):
     return step
 
 
+def run_e2e_peer(torch, dev, w, world, rank, calls, args):
+    """e2e at N>1 through DistributedSlabs: every step uploads this rank's slab of phi / speed /
+    state from pinned host memory, solves, and downloads its phi slab; wall time max over ranks."""
+    import torch.distributed as dist
+
+    from paper_2106_15869_b200.slab import SlabPartition
+    from paper_2106_15869_b200.slab_peer import DistributedSlabs
+
+    n = w.n
+    z0, z1 = SlabPartition(n, world).bounds(rank)
+    ds = DistributedSlabs((n, n, n), w.h)
+    sp_h = w.F[z0:z1].cpu().pin_memory()
+    phi_h = torch.full((z1 - z0, n, n), float("inf"), dtype=torch.float64).pin_memory()
+    st_h = torch.zeros((z1 - z0, n, n), dtype=torch.uint8).pin_memory()
+    out_h = torch.empty_like(phi_h).pin_memory()
+    sp = torch.empty(sp_h.shape, dtype=torch.float64, device=dev)
+    st = torch.empty(st_h.shape, dtype=torch.uint8, device=dev)
+    seeds = w.linear_seeds()
+    steps = max(1, min(args.steps, 3))
+    tot = 0.0
+    for it in range(steps + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        sp.copy_(sp_h, non_blocking=True)
+        st.copy_(st_h, non_blocking=True)
+        phi, s = ds.solve(sp, st, seeds, phi_local=phi_h)
+        out_h.copy_(phi, non_blocking=True)
+        torch.cuda.synchronize()
+        dt = torch.tensor([time.perf_counter() - t0], device=dev)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        assert s.solver_calls == calls
+        if it > 0:
+            tot += float(dt.item())
+    per = (z1 - z0) * n * n
+    return {"value": calls * steps / tot, "unit": UNIT, "h2d_bytes_per_step": per * (8 + 8 + 1),
+            "d2h_bytes_per_step": per * 8, "steps": steps, "ms_per_step": tot / steps * 1e3,
+            "note": "per rank (rank 0's slab); wall time max over ranks"}
+
+
 def run_ours(args):
     import torch
 
@@ -499,10 +539,20 @@ def run_ours(args):
     traffic = traffic_from_profiles(workload) if not slabs and args.dtype == "f64" and args.method == "ifim" else None
 
     out = None
+    e2e_peer = None
+    if mode == "peer" and not args.no_e2e:  # collective: every rank takes part
+        try:
+            e2e_peer = run_e2e_peer(torch, dev, w, world, rank, calls, args)
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] peer e2e failed on rank {rank}: {e!r}", file=sys.stderr, flush=True)
     if rank == 0:
-        e2e = run_e2e(eik, torch, dev, w, calls, args, rdt) if not (slabs or args.no_e2e or args.method == "fim") else \
-            {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-             "note": "e2e is measured by the single-GPU run through solve_ifim"}
+        if e2e_peer is not None:
+            e2e = e2e_peer
+        elif not (slabs or args.no_e2e or args.method == "fim"):
+            e2e = run_e2e(eik, torch, dev, w, calls, args, rdt)
+        else:
+            e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                   "note": "e2e is measured by the single-GPU run through solve_ifim"}
         cpu_calls, cpu_s = cpu_sample(args.cpu_size, os.cpu_count() or 1, args.config) if not args.no_cpu \
             else (0, 0.0)
         out = {

@@ -130,11 +130,16 @@ class DistributedSlabs:
         z0, z1 = self.bounds[self.rank]
         self.phi = self.buf[: (z1 - z0) * ny * nx * 8].view(torch.float64).view(z1 - z0, ny, nx)
 
-    def solve(self, speed_local, state_local, seeds, tol=1e-12):
+    def solve(self, speed_local, state_local, seeds, tol=1e-12, phi_local=None):
+        """speed/state: this rank's planes (device); phi_local: its starting phi planes (any
+        device, default +inf).  Returns (this rank's phi planes, global RunStats)."""
         import torch.distributed as dist
 
         nz, ny, nx = self.shape
-        self.phi.fill_(INF)
+        if phi_local is None:
+            self.phi.fill_(INF)
+        else:
+            self.phi.copy_(phi_local, non_blocking=True)
         spp = (C.c_void_p * 1)(speed_local.data_ptr())
         stp = (C.c_void_p * 1)(state_local.data_ptr())
         si = torch.as_tensor([c for c, _ in seeds], dtype=torch.int64, device=self.dev)
