@@ -301,9 +301,16 @@ def make_single_step(eik, torch, dev, w, dtype):
         r = eik.solve_ifim(g, bc)
         s = r.stats
         ph = s.phases
-        rem_writes = s.phi_writes - (ph["update"]["solver_calls"] - ph["update"]["converged"])
-        return StepStats(s.solver_calls, s.iterations, s.peak_remedy, ph["remedy"]["solver_calls"], rem_writes,
-                         s.device_ms["remedy"], s.gpu_launches, {k: round(v, 3) for k, v in s.device_ms.items()})
+        upd_writes = ph["update"]["solver_calls"] - ph["update"]["converged"]
+        rem_writes = s.phi_writes - upd_writes
+        st_ = StepStats(s.solver_calls, s.iterations, s.peak_remedy, ph["remedy"]["solver_calls"], rem_writes,
+                        s.device_ms["remedy"], s.gpu_launches, {k: round(v, 3) for k, v in s.device_ms.items()})
+        # per-phase algorithmic bytes (8 B x (2 calls + writes); build: 2 x 8 B per free cell)
+        rs = phi.element_size()
+        st_.phase_bytes = {"update": rs * (2 * ph["update"]["solver_calls"] + upd_writes),
+                           "build": rs * 2 * ph["build"]["solver_calls"],
+                           "remedy": rs * (2 * ph["remedy"]["solver_calls"] + rem_writes)}
+        return st_
 
     return step
 
@@ -398,9 +405,16 @@ def make_peer_step(torch, dev, w, world, rank):
         st.copy_(st0)
         _, s = ds.solve(sp, st, seeds)
         ph = s.phases
-        rem_writes = s.phi_writes - (ph["update"]["solver_calls"] - ph["update"]["converged"])
-        return StepStats(s.solver_calls, s.iterations, s.peak_remedy, ph["remedy"]["solver_calls"], rem_writes,
-                         s.device_ms["remedy"], s.gpu_launches, {k: round(v, 3) for k, v in s.device_ms.items()})
+        upd_writes = ph["update"]["solver_calls"] - ph["update"]["converged"]
+        rem_writes = s.phi_writes - upd_writes
+        st_ = StepStats(s.solver_calls, s.iterations, s.peak_remedy, ph["remedy"]["solver_calls"], rem_writes,
+                        s.device_ms["remedy"], s.gpu_launches, {k: round(v, 3) for k, v in s.device_ms.items()})
+        # per-phase algorithmic bytes (8 B x (2 calls + writes); build: 2 x 8 B per free cell)
+        rs = phi.element_size()
+        st_.phase_bytes = {"update": rs * (2 * ph["update"]["solver_calls"] + upd_writes),
+                           "build": rs * 2 * ph["build"]["solver_calls"],
+                           "remedy": rs * (2 * ph["remedy"]["solver_calls"] + rem_writes)}
+        return st_
 
     return step
 
@@ -572,6 +586,9 @@ def run_ours(args):
                          "kernel": "k_fim" if args.method == "fim" else "k_remedy", "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": rem_s * 1e3,
                          "peak_source": peak_src},
+            "phase_roofline": ({k: round(b / (r.phase_ms[k] * 1e-3) / 1e9 / hbm_peak()[0], 4)
+                                for k, b in r.phase_bytes.items() if r.phase_ms.get(k)}
+                               if getattr(r, "phase_bytes", None) else None),
             "cpu_baseline": {"value": (cpu_calls / cpu_s) if cpu_s else None, "unit": UNIT,
                              "cores": os.cpu_count() or 1, "kind": "port",
                              "sample": f"full solve of {workload_desc(args.config, args.cpu_size)} (same family) with "
