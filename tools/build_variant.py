@@ -1,5 +1,5 @@
 """Build an experiment variant of the engine: python tools/build_variant.py NAME [-DMACRO[=V] ...]
--> paper_2106_15869_b200/NAME.so (load it with tools/mu_sweep.py NAME.so / diag_density.py)."""
+-> paper_2106_15869_b200/NAME.so (compare with tools/ab.py NAME.so ..., diagnostics: tools/diag_density.py)."""
 import os
 import subprocess
 import sys
