@@ -860,6 +860,9 @@ __device__ __forceinline__ void update_body(const KP &p)
                                 if (!(old2 & bit)) {
                                     uint32_t *Lp = par ? pr.L0 : pr.L1;
                                     Lp[atomicAdd_system(&pr.ctl->len[(it + 1) % 3], 1u)] = (ze * ny + y[u]) * nx + x[u];
+                                    // the only remote plain store: publish it system-wide before this
+                                    // CTA arrives at the (gpu-scope) barrier
+                                    __threadfence_system();
                                 }
                             }
                             continue;
