@@ -107,6 +107,7 @@ struct Ctl {
     unsigned wcount;                // multi-rank: world-barrier arrivals (rank 0's copy is used)
     unsigned wgen;                  // multi-rank: this rank's world-barrier generation
     unsigned fc[3];                 // FIM: check-list length per rotating slot
+    unsigned gcount[64];            // grid barrier: arrivals per group of BAR_GROUP CTAs
 #ifdef EIK_DIAG
     unsigned long long dg[4][26];   // remedy rounds by log2|R_r|: count, phase B ns, phase A ns, members
     unsigned long long du[3][26];   // update iterations by log2|A_k|: count, ns, cells
@@ -366,6 +367,12 @@ __device__ __forceinline__ bool spin_until_change(volatile unsigned *w, unsigned
     return true;
 }
 
+#ifndef BAR_GROUP
+#define BAR_GROUP 32  // CTAs per first-level barrier group (<= 64 groups)
+#endif
+#ifndef BAR_TREE_MIN
+#define BAR_TREE_MIN 512  // grids up to this many CTAs arrive on one counter (measured faster)
+#endif
 __device__ __forceinline__ bool grid_barrier_n(Ctl *ctl, unsigned nblocks, const KP *p)
 {
     __shared__ unsigned s_ok;
@@ -377,9 +384,23 @@ __device__ __forceinline__ bool grid_barrier_n(Ctl *ctl, unsigned nblocks, const
         // acquires every CTA's arrival, then publishes system-wide (fence.sc.sys
         // before the cross-rank atomic), and causality order is transitive
         __threadfence();
-        const unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
+        // two-level arrival: CTAs count in groups of BAR_GROUP, the last of each group counts
+        // at the top, so no single address takes every CTA's atomic
+        const unsigned gi = blockIdx.x - (p ? p->gb0 : 0u);
+        const unsigned grp = gi / BAR_GROUP;
+        const unsigned ngrp = nblocks > BAR_TREE_MIN ? (nblocks + BAR_GROUP - 1) / BAR_GROUP : 1u;
+        const unsigned gsz = min((unsigned)BAR_GROUP, nblocks - grp * BAR_GROUP);
+        bool top = true;
+        if (ngrp > 1) {
+            top = atomicAdd(&ctl->gcount[grp], 1u) == gsz - 1;
+            if (top) {
+                atomicExch(&ctl->gcount[grp], 0u);
+                __threadfence();
+            }
+        }
+        const unsigned arrived = top ? atomicAdd(&ctl->bar_count, 1u) : 0u;
         unsigned ok = 1;
-        if (arrived == nblocks - 1) {
+        if (top && arrived == (ngrp > 1 ? ngrp : nblocks) - 1) {
             atomicExch(&ctl->bar_count, 0u);
             if (p && p->mr && p->R > 1) {
                 volatile unsigned *wg = &ctl->wgen;
