@@ -89,8 +89,6 @@ __device__ __forceinline__ real_t real_of_bits(unsigned long long b)
 }
 
 struct Ctl {
-    unsigned bar_count;
-    unsigned bar_gen;
     unsigned len[3];
     unsigned err;
     unsigned long long cnt[3];
@@ -107,7 +105,12 @@ struct Ctl {
     unsigned wcount;                // multi-rank: world-barrier arrivals (rank 0's copy is used)
     unsigned wgen;                  // multi-rank: this rank's world-barrier generation
     unsigned fc[3];                 // FIM: check-list length per rotating slot
-    unsigned gcount[64];            // grid barrier: arrivals per group of BAR_GROUP CTAs
+    // grid barrier words, each on its own 128-byte line (arrivals do not share a line with
+    // the generation word every waiting CTA polls, nor with the round counters)
+    alignas(128) unsigned bar_count;
+    alignas(128) unsigned bar_gen;
+    struct alignas(128) Line { unsigned v; };
+    Line gcount[64];                // arrivals per group of BAR_GROUP CTAs
 #ifdef EIK_DIAG
     unsigned long long dg[4][26];   // remedy rounds by log2|R_r|: count, phase B ns, phase A ns, members
     unsigned long long du[3][26];   // update iterations by log2|A_k|: count, ns, cells
@@ -357,9 +360,10 @@ constexpr unsigned EIK_EHANG = 5;  // device-side watchdog tripped (reported as 
 __device__ __forceinline__ bool spin_until_change(volatile unsigned *w, unsigned old, Ctl *ctl)
 {
     const unsigned long long t0 = globaltimer();
-    while (*w == old) {
+    for (unsigned k = 0; *w == old; ++k) {
         __nanosleep(32);
-        if (*(volatile unsigned *)&ctl->err == EIK_EHANG || globaltimer() - t0 > 10000000000ull) {
+        if ((k & 15u) == 15u &&  // watchdog checks every 16 polls
+            (*(volatile unsigned *)&ctl->err == EIK_EHANG || globaltimer() - t0 > 10000000000ull)) {
             atomicExch(&ctl->err, EIK_EHANG);
             return false;
         }
@@ -392,9 +396,9 @@ __device__ __forceinline__ bool grid_barrier_n(Ctl *ctl, unsigned nblocks, const
         const unsigned gsz = min((unsigned)BAR_GROUP, nblocks - grp * BAR_GROUP);
         bool top = true;
         if (ngrp > 1) {
-            top = atomicAdd(&ctl->gcount[grp], 1u) == gsz - 1;
+            top = atomicAdd(&ctl->gcount[grp].v, 1u) == gsz - 1;
             if (top) {
-                atomicExch(&ctl->gcount[grp], 0u);
+                atomicExch(&ctl->gcount[grp].v, 0u);
                 __threadfence();
             }
         }
