@@ -357,11 +357,14 @@ constexpr unsigned EIK_EHANG = 5;  // device-side watchdog tripped (reported as 
 // the data written before the barrier visible to peer GPUs.  Returns false if
 // the watchdog fired (nobody arrived within ~10 s); callers then leave the
 // kernel so a logic error cannot wedge the GPU.
+#ifndef SPIN_NS
+#define SPIN_NS 32  // back-off between polls of a barrier word
+#endif
 __device__ __forceinline__ bool spin_until_change(volatile unsigned *w, unsigned old, Ctl *ctl)
 {
     const unsigned long long t0 = globaltimer();
     for (unsigned k = 0; *w == old; ++k) {
-        __nanosleep(32);
+        if (SPIN_NS) __nanosleep(SPIN_NS);
         if ((k & 15u) == 15u &&  // watchdog checks every 16 polls
             (*(volatile unsigned *)&ctl->err == EIK_EHANG || globaltimer() - t0 > 10000000000ull)) {
             atomicExch(&ctl->err, EIK_EHANG);
