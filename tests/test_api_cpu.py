@@ -144,3 +144,38 @@ def test_resolve_devices(monkeypatch):
     assert resolve_devices(None) == [0, 1]
     monkeypatch.setenv("EIKONAL_DEVICES", "0,0,2")
     assert resolve_devices(None) == [0, 0, 2]
+
+
+def test_field_csv_round_trip_is_bit_exact(tmp_path):
+    """T/test_harness.py:111-121 against E/harness.py:326-380's format."""
+    g = eik.new_grid(5, 3, 0.1, 0.7, origin=(0.3, -1.0))
+    rng = np.random.default_rng(1)
+    g.phi[:] = rng.random((3, 5))
+    g.phi[1, 2] = np.inf
+    p = str(tmp_path / "f.csv")
+    eik.export_field_csv(g, p)
+    h = eik.import_field_csv(p)
+    assert (h.nx, h.ny, h.dx, h.dy, h.origin) == (5, 3, 0.1, 0.7, (0.3, -1.0))
+    assert np.array_equal(h.phi.view(np.uint64), g.phi.view(np.uint64))
+    with open(p) as fh:
+        lines = fh.read().splitlines()
+    with open(p, "w") as fh:
+        fh.write("\n".join(lines[:-1]) + "\n")
+    with pytest.raises(ValueError):
+        eik.import_field_csv(p)
+
+
+def test_field_npy_round_trip_3d(tmp_path):
+    """Binary snapshot for fields too large for CSV."""
+    g = eik.new_grid_3d(7, 5, 4, 0.25, origin=(1.0, 2.0, 3.0))
+    g.phi[:] = np.random.default_rng(2).random((4, 5, 7))
+    g.phi[0, 0, 0] = np.inf
+    p = str(tmp_path / "f.npy")
+    eik.export_field_npy(g, p)
+    h = eik.import_field_npy(p)
+    assert isinstance(h, eik.Grid3D) and (h.nx, h.ny, h.nz, h.h, h.origin) == (7, 5, 4, 0.25, (1.0, 2.0, 3.0))
+    assert np.array_equal(h.phi.view(np.uint64), g.phi.view(np.uint64)) and (h.state == 0).all()
+    t = eik.Grid3D(7, 5, 4, 0.25, (0.0, 0.0, 0.0), torch.from_numpy(g.phi.copy()), torch.ones((4, 5, 7)),
+                   torch.zeros((4, 5, 7), dtype=torch.uint8))
+    eik.export_field_npy(t, p)
+    assert np.array_equal(np.load(p).view(np.uint64), g.phi.view(np.uint64))

@@ -130,3 +130,17 @@ def test_cfg5_full_size_ifim_equals_fixpoint():
     g.state.zero_()
     b = eik.solve_fixpoint(g, bc).phi
     assert eik.field_max_diff(a, b) <= 1e-9
+
+
+def test_field_npy_streams_a_device_field(tmp_path):
+    """export_field_npy / import_field_npy on a CUDA field (chunked D2H / H2D), bit-exact."""
+    n = 96
+    g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), np.inf, dtype=torch.float64, device="cuda"),
+                   torch.ones((n, n, n), dtype=torch.float64, device="cuda"),
+                   torch.zeros((n, n, n), dtype=torch.uint8, device="cuda"))
+    res = eik.solve_ifim(g, eik.seed_point(g, (10, 20, 30), 0.0))
+    p = str(tmp_path / "phi.npy")
+    eik.export_field_npy(g, p)
+    h = eik.import_field_npy(p, device="cuda")
+    assert torch.equal(h.phi, res.phi) and h.phi.is_cuda
+    assert eik.field_sha256(np.load(p)) == eik.field_sha256(res.phi)
