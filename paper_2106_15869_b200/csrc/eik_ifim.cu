@@ -1900,7 +1900,9 @@ struct Engine {
     }
     static int update(KP &p, cudaStream_t st)
     {
-        return coop_launch(k_update<DIM, SOL>, p, nullptr, false, st, "EIK_UPD_BLOCKS_PER_SM", 0);
+        // 2D fronts are O(n) cells: one CTA per SM keeps the per-iteration barrier cheap
+        // (cfg2 4096^2: 29 vs 34 ms); 3D fronts are O(n^2) and want the full occupancy
+        return coop_launch(k_update<DIM, SOL>, p, nullptr, false, st, "EIK_UPD_BLOCKS_PER_SM", DIM == 2 ? 1 : 0);
     }
     // remedy-set slots: counters (R0 is rewritten word by word)
     static int reset_set(KP &p, cudaStream_t st)
