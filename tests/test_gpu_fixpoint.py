@@ -1,5 +1,7 @@
 """GPU fixpoint / residual vs the CPU restatement and the
 reference's own fixpoint output, plus full-size properties of the iFIM field."""
+import math
+
 import numpy as np
 import pytest
 import torch
@@ -144,3 +146,30 @@ def test_field_npy_streams_a_device_field(tmp_path):
     h = eik.import_field_npy(p, device="cuda")
     assert torch.equal(h.phi, res.phi) and h.phi.is_cuda
     assert eik.field_sha256(np.load(p)) == eik.field_sha256(res.phi)
+
+
+@pytest.mark.slow
+def test_near_max_grid_1280_cubed():
+    """Near the 2^31-cells-per-device limit (1280^3 = 2.1e9 cells, ~100 GB on the device): a
+    corner source on a cubic grid gives a field that is bitwise symmetric under axis
+    permutations (the solver sorts its three axis minima; Jacobi sets are order-free), finite
+    everywhere, and within first-order error of the distance at the far corner."""
+    n = 1280
+    dev = torch.device("cuda:0")
+    g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), np.inf, dtype=torch.float64, device=dev),
+                   torch.ones((n, n, n), dtype=torch.float64, device=dev),
+                   torch.zeros((n, n, n), dtype=torch.uint8, device=dev))
+    try:
+        r = eik.solve_ifim(g, eik.seed_point(g, (0, 0, 0), 0.0))
+        phi = g.phi
+        del r
+        assert bool(torch.isfinite(phi).all())
+        for a, b in ((0, 2), (1, 2), (0, 1)):
+            assert torch.equal(phi, phi.transpose(a, b)), (a, b)
+        far = float(phi[n - 1, n - 1, n - 1])
+        exact = math.sqrt(3.0) * (n - 1)
+        assert exact <= far <= exact * 1.05
+    finally:
+        del g
+        eik.clear_workspaces()
+        torch.cuda.empty_cache()
