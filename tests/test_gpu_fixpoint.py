@@ -156,6 +156,8 @@ def test_near_max_grid_1280_cubed():
     everywhere, and within first-order error of the distance at the far corner."""
     n = 1280
     dev = torch.device("cuda:0")
+    eik.clear_workspaces()  # earlier full-size tests may still hold cached workspaces / blocks
+    torch.cuda.empty_cache()
     g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), np.inf, dtype=torch.float64, device=dev),
                    torch.ones((n, n, n), dtype=torch.float64, device=dev),
                    torch.zeros((n, n, n), dtype=torch.uint8, device=dev))
