@@ -3,32 +3,38 @@
 // Implements the C ABI declared in include/eik_ifim.h.  The reference path it
 // replaces is E/ifim.py (E = /root/reference/pkg/src/eikonal):
 //
-//   update step  (E/ifim.py:75-134)  -> k_update   persistent, push/worklist
-//   build pass   (E/ifim.py:137-161) -> k_build    one streaming pass
-//   remedy step  (E/ifim.py:164-218) -> k_remedy   persistent, pull/bitmap
+//   update step  (E/ifim.py:75-134)  -> k_update   persistent, one thread per active cell
+//   build pass   (E/ifim.py:137-161) -> k_build    one pass, one warp per bitmap word
+//   remedy step  (E/ifim.py:164-218) -> k_remedy   persistent; per round the member list is
+//                                                  rebuilt from the decrease bitmap, then one
+//                                                  thread per member
+// plus the fixpoint ground truth (E/oracle.py, k_fixpoint), max_residual
+// (E/harness.py, k_residual), the FIM baseline (E/fim.py, k_fim) and the
+// multi-rank z-slab variants of the update / remedy kernels (peer memory).
 //
 // Data layout in HBM:
-//   * phi: the caller's float64 array (row-major, x fastest) plus one
-//     workspace copy.  The two form a Jacobi double buffer: iteration k reads
-//     P[k&1] and every processed cell writes its final value into P[(k+1)&1],
-//     which keeps the snapshot semantics of padded_phi (E/_kernels.py:21-26)
-//     without any O(N) copy per iteration.  At termination both are equal.
+//   * phi: the caller's array (row-major, x fastest) plus one workspace copy.
+//     The two form a Jacobi double buffer: iteration k reads P[k&1]; every
+//     processed cell whose value changes, or changed in iteration k-1 (CARRY
+//     bit of its list entry), writes P[(k+1)&1].  That keeps the snapshot
+//     semantics of padded_phi (E/_kernels.py:21-26) without an O(N) copy per
+//     iteration; at termination both buffers are equal.
 //   * d = delta / F precomputed per cell (bit-identical to the per-call
 //     division at E/_kernels.py:48 and E/local_solver.py:105).
 //   * Sets are bitmaps with one 32-bit word per 32 consecutive cells of one
-//     x-row (word w <-> row w / W, lanes x = 32*(w % W) + lane); a warp owns a
-//     word, lane = cell.  Rows are padded to whole words.
-//   * Worklists are compacted lists of non-empty words.
+//     x-row (word w <-> row w / W, x = 32*(w % W) + bit); rows are padded to
+//     whole words.  Worklists hold cell indices (< 2^31, bit 31 = CARRY).
 //
-// Arithmetic is float64 IEEE with FMA contraction disabled (-fmad=false) and
-// the reference's operation order, so phi is bit-identical to the reference
-// and every RunStats integer (iterations, solver_calls, peaks, active_history)
-// matches exactly.
+// Arithmetic is IEEE with FMA contraction disabled (-fmad=false) and the
+// reference's operation order, so the float64 build is bit-identical to the
+// reference: phi and every RunStats integer (iterations, solver_calls, peaks,
+// active_history).  The same source compiled with -DEIK_SINGLE=1 is the
+// float32 perf mode (names suffixed _f32).
 //
 // Termination is device-side: the persistent kernels loop over iterations
 // with a software grid barrier (co-residency guaranteed by a cooperative
-// launch) and read the global set size after each barrier; the host sees only
-// the final statistics.
+// launch, 10 s watchdog) and read the global set size after each barrier;
+// the host sees only the final statistics.
 
 #include <cuda_runtime.h>
 
