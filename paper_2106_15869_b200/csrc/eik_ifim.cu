@@ -1088,7 +1088,9 @@ __global__ void k_remedy_export(KP p, uint8_t *member)
 // |R_r| is the list length, |D_r| a counter; the loop ends when D_r is empty.
 // ---------------------------------------------------------------------------
 
-constexpr int REM_PER = 4;  // bitmap words per thread in phase B
+#ifndef REM_PER
+#define REM_PER 4  // bitmap words per thread in phase B
+#endif
 #ifndef REM_MU
 #define REM_MU 2            // phase A: members per lane in flight
 #endif
