@@ -386,36 +386,74 @@ __device__ __forceinline__ bool spin_until_change(volatile unsigned *w, unsigned
 #ifndef BAR_TREE_MIN
 #define BAR_TREE_MIN 512  // grids up to this many CTAs arrive on one counter (measured faster)
 #endif
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned *a, unsigned v)
+{
+    unsigned old;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void red_add_release_gpu(unsigned *a, unsigned v)
+{
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *a)
+{
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+    return v;
+}
+
+// Software grid barrier over the nblocks CTAs of this rank (and, in multi-rank
+// mode, across ranks).  Thread 0 of each CTA arrives with an acq_rel atomic
+// (releasing the CTA's writes, ordered before it by bar.sync), the last arriver
+// releases the generation word and the others acquire it; the watchdog turns a
+// missing arrival into EIK_EHANG instead of a wedged GPU.
 __device__ __forceinline__ bool grid_barrier_n(Ctl *ctl, unsigned nblocks, const KP *p)
 {
     __shared__ unsigned s_ok;
     __syncthreads();
+    if (!p || !p->mr) {
+        // single rank: one acq_rel add per CTA on one word; CTA 0 adds 2^31 - (n - 1), the others
+        // 1, so the last arrival flips bit 31 and leaves the low bits as they were (no reset, no
+        // separate release); everyone waits for the flip with acquire loads
+        if (threadIdx.x == 0) {
+            const unsigned add = blockIdx.x == (p ? p->gb0 : 0u) ? 0x80000000u - (nblocks - 1u) : 1u;
+            const unsigned old = atom_add_acq_rel_gpu(&ctl->bar_count, add);
+            unsigned ok = 1;
+            const unsigned long long t0 = globaltimer();
+            for (unsigned k = 0; ((old ^ ld_acquire_gpu(&ctl->bar_count)) & 0x80000000u) == 0u; ++k) {
+                if (SPIN_NS) __nanosleep(SPIN_NS);
+                if ((k & 15u) == 15u &&  // watchdog checks every 16 polls
+                    (*(volatile unsigned *)&ctl->err == EIK_EHANG || globaltimer() - t0 > 10000000000ull)) {
+                    atomicExch(&ctl->err, EIK_EHANG);
+                    ok = 0;
+                    break;
+                }
+            }
+            s_ok = ok;
+        }
+        __syncthreads();
+        return s_ok != 0;
+    }
     if (threadIdx.x == 0) {
-        volatile unsigned *vgen = &ctl->bar_gen;
-        const unsigned gen = *vgen;
-        // gpu-scope release is enough here even across ranks: the last arriver
-        // acquires every CTA's arrival, then publishes system-wide (fence.sc.sys
-        // before the cross-rank atomic), and causality order is transitive
-        __threadfence();
-        // two-level arrival: CTAs count in groups of BAR_GROUP, the last of each group counts
-        // at the top, so no single address takes every CTA's atomic
+        const unsigned gen = *(volatile unsigned *)&ctl->bar_gen;
+        // two-level arrival for large grids: CTAs count in groups of BAR_GROUP, the last of each
+        // group counts at the top, so no single address takes every CTA's atomic
         const unsigned gi = blockIdx.x - (p ? p->gb0 : 0u);
         const unsigned grp = gi / BAR_GROUP;
         const unsigned ngrp = nblocks > BAR_TREE_MIN ? (nblocks + BAR_GROUP - 1) / BAR_GROUP : 1u;
         const unsigned gsz = min((unsigned)BAR_GROUP, nblocks - grp * BAR_GROUP);
         bool top = true;
         if (ngrp > 1) {
-            top = atomicAdd(&ctl->gcount[grp].v, 1u) == gsz - 1;
-            if (top) {
-                atomicExch(&ctl->gcount[grp].v, 0u);
-                __threadfence();
-            }
+            top = atom_add_acq_rel_gpu(&ctl->gcount[grp].v, 1u) == gsz - 1;
+            if (top) atomicExch(&ctl->gcount[grp].v, 0u);
         }
-        const unsigned arrived = top ? atomicAdd(&ctl->bar_count, 1u) : 0u;
+        const unsigned arrived = top ? atom_add_acq_rel_gpu(&ctl->bar_count, 1u) : 0u;
         unsigned ok = 1;
         if (top && arrived == (ngrp > 1 ? ngrp : nblocks) - 1) {
             atomicExch(&ctl->bar_count, 0u);
             if (p && p->mr && p->R > 1) {
+                // cross-rank level: publish system-wide, count at rank 0, wait for the world
                 volatile unsigned *wg = &ctl->wgen;
                 const unsigned wgen = *wg;
                 __threadfence_system();
@@ -429,13 +467,20 @@ __device__ __forceinline__ bool grid_barrier_n(Ctl *ctl, unsigned nblocks, const
                 }
                 __threadfence_system();
             }
-            __threadfence();
-            atomicAdd(&ctl->bar_gen, 1u);
+            red_add_release_gpu(&ctl->bar_gen, 1u);
         } else {
-            ok = spin_until_change(vgen, gen, ctl);
+            const unsigned long long t0 = globaltimer();
+            for (unsigned k = 0; ld_acquire_gpu(&ctl->bar_gen) == gen; ++k) {
+                if (SPIN_NS) __nanosleep(SPIN_NS);
+                if ((k & 15u) == 15u &&  // watchdog checks every 16 polls
+                    (*(volatile unsigned *)&ctl->err == EIK_EHANG || globaltimer() - t0 > 10000000000ull)) {
+                    atomicExch(&ctl->err, EIK_EHANG);
+                    ok = 0;
+                    break;
+                }
+            }
         }
-        __threadfence();
-        s_ok = ok && *(volatile unsigned *)&ctl->err != EIK_EHANG;
+        s_ok = ok;
     }
     __syncthreads();
     return s_ok != 0;
