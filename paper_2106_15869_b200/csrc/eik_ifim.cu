@@ -111,12 +111,10 @@ struct Ctl {
     unsigned wcount;                // multi-rank: world-barrier arrivals (rank 0's copy is used)
     unsigned wgen;                  // multi-rank: this rank's world-barrier generation
     unsigned fc[3];                 // FIM: check-list length per rotating slot
-    // grid barrier words, each on its own 128-byte line (arrivals do not share a line with
-    // the generation word every waiting CTA polls, nor with the round counters)
+    // grid barrier word on its own 128-byte line (the arrivals and the polls do not share a
+    // line with the round counters)
     alignas(128) unsigned bar_count;
-    alignas(128) unsigned bar_gen;
-    struct alignas(128) Line { unsigned v; };
-    Line gcount[64];                // arrivals per group of BAR_GROUP CTAs
+    alignas(128) unsigned bar_gen;  // multi-rank release generation
 #ifdef EIK_DIAG
     unsigned long long dg[4][26];   // remedy rounds by log2|R_r|: count, phase B ns, phase A ns, members
     unsigned long long du[3][26];   // update iterations by log2|A_k|: count, ns, cells
@@ -380,21 +378,11 @@ __device__ __forceinline__ bool spin_until_change(volatile unsigned *w, unsigned
     return true;
 }
 
-#ifndef BAR_GROUP
-#define BAR_GROUP 32  // CTAs per first-level barrier group (<= 64 groups)
-#endif
-#ifndef BAR_TREE_MIN
-#define BAR_TREE_MIN 512  // grids up to this many CTAs arrive on one counter (measured faster)
-#endif
 __device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned *a, unsigned v)
 {
     unsigned old;
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(a), "r"(v) : "memory");
     return old;
-}
-__device__ __forceinline__ void red_add_release_gpu(unsigned *a, unsigned v)
-{
-    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *a)
 {
@@ -412,7 +400,7 @@ __device__ __forceinline__ bool grid_barrier_n(Ctl *ctl, unsigned nblocks, const
 {
     __shared__ unsigned s_ok;
     __syncthreads();
-    if (!p || !p->mr) {
+    if (!p || !p->mr || p->R == 1) {
         // single rank: one acq_rel add per CTA on one word; CTA 0 adds 2^31 - (n - 1), the others
         // 1, so the last arrival flips bit 31 and leaves the low bits as they were (no reset, no
         // separate release); everyone waits for the flip with acquire loads
@@ -435,51 +423,34 @@ __device__ __forceinline__ bool grid_barrier_n(Ctl *ctl, unsigned nblocks, const
         __syncthreads();
         return s_ok != 0;
     }
+    // multi-rank: arrivals count on bar_count; the rank's last arriver meets the other ranks
+    // (system-scope counter at rank 0, then every rank's wgen) and releases its rank through the
+    // generation word bar_gen, which the others poll
     if (threadIdx.x == 0) {
-        const unsigned gen = *(volatile unsigned *)&ctl->bar_gen;
-        // two-level arrival for large grids: CTAs count in groups of BAR_GROUP, the last of each
-        // group counts at the top, so no single address takes every CTA's atomic
-        const unsigned gi = blockIdx.x - (p ? p->gb0 : 0u);
-        const unsigned grp = gi / BAR_GROUP;
-        const unsigned ngrp = nblocks > BAR_TREE_MIN ? (nblocks + BAR_GROUP - 1) / BAR_GROUP : 1u;
-        const unsigned gsz = min((unsigned)BAR_GROUP, nblocks - grp * BAR_GROUP);
-        bool top = true;
-        if (ngrp > 1) {
-            top = atom_add_acq_rel_gpu(&ctl->gcount[grp].v, 1u) == gsz - 1;
-            if (top) atomicExch(&ctl->gcount[grp].v, 0u);
-        }
-        const unsigned arrived = top ? atom_add_acq_rel_gpu(&ctl->bar_count, 1u) : 0u;
+        volatile unsigned *vgen = &ctl->bar_gen;
+        const unsigned gen = *vgen;
+        __threadfence();  // gpu-scope release; the last arriver publishes system-wide below
         unsigned ok = 1;
-        if (top && arrived == (ngrp > 1 ? ngrp : nblocks) - 1) {
+        if (atomicAdd(&ctl->bar_count, 1u) == nblocks - 1u) {
             atomicExch(&ctl->bar_count, 0u);
-            if (p && p->mr && p->R > 1) {
-                // cross-rank level: publish system-wide, count at rank 0, wait for the world
-                volatile unsigned *wg = &ctl->wgen;
-                const unsigned wgen = *wg;
+            volatile unsigned *wg = &ctl->wgen;
+            const unsigned wgen = *wg;
+            __threadfence_system();
+            Ctl *c0 = p->rank_ctl[0];
+            if (atomicAdd_system(&c0->wcount, 1u) == (unsigned)p->R - 1) {
+                atomicExch_system(&c0->wcount, 0u);
                 __threadfence_system();
-                Ctl *c0 = p->rank_ctl[0];
-                if (atomicAdd_system(&c0->wcount, 1u) == (unsigned)p->R - 1) {
-                    atomicExch_system(&c0->wcount, 0u);
-                    __threadfence_system();
-                    for (int r = 0; r < p->R; ++r) atomicAdd_system(&p->rank_ctl[r]->wgen, 1u);
-                } else {
-                    ok = spin_until_change(wg, wgen, ctl);
-                }
-                __threadfence_system();
+                for (int r = 0; r < p->R; ++r) atomicAdd_system(&p->rank_ctl[r]->wgen, 1u);
+            } else {
+                ok = spin_until_change(wg, wgen, ctl);
             }
-            red_add_release_gpu(&ctl->bar_gen, 1u);
+            __threadfence_system();
+            __threadfence();
+            atomicAdd(&ctl->bar_gen, 1u);
         } else {
-            const unsigned long long t0 = globaltimer();
-            for (unsigned k = 0; ld_acquire_gpu(&ctl->bar_gen) == gen; ++k) {
-                if (SPIN_NS) __nanosleep(SPIN_NS);
-                if ((k & 15u) == 15u &&  // watchdog checks every 16 polls
-                    (*(volatile unsigned *)&ctl->err == EIK_EHANG || globaltimer() - t0 > 10000000000ull)) {
-                    atomicExch(&ctl->err, EIK_EHANG);
-                    ok = 0;
-                    break;
-                }
-            }
+            ok = spin_until_change(vgen, gen, ctl);
         }
+        __threadfence();
         s_ok = ok;
     }
     __syncthreads();
