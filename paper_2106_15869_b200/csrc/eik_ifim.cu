@@ -826,6 +826,7 @@ __device__ __forceinline__ void update_body(const KP &p)
         }
     }
     const uint32_t nx = (uint32_t)p.nx, ny = (uint32_t)p.ny, nz = (uint32_t)p.nz;
+    unsigned nnext = ~0u;  // next iteration's list length when already read
     for (int64_t it = p.it0; it < p.it0 + p.max_it; ++it) {
         const int par = (int)(it & 1);
         const real_t *__restrict__ Pc = par ? p.P1 : p.P0;
@@ -833,7 +834,8 @@ __device__ __forceinline__ void update_body(const KP &p)
         const uint32_t *__restrict__ Lc = par ? p.L1 : p.L0;
         uint32_t *Ln = par ? p.L0 : p.L1;
         unsigned *lenN = &ctl->len[(it + 1) % 3];
-        const unsigned n = vload(&ctl->len[it % 3]);
+        // this rank's list length (single rank: the global count read after the last barrier)
+        const unsigned n = nnext != ~0u ? nnext : vload(&ctl->len[it % 3]);
         for (unsigned base = gb * (BLOCK * UPD_MU); base < n; base += gnb * (BLOCK * UPD_MU)) {
             uint32_t c[UPD_MU], x[UPD_MU], y[UPD_MU], z[UPD_MU], r[UPD_MU];
             unsigned emit[UPD_MU];  // bit 0: stay; bits 1..6: activate W, E, S, N, D, U
@@ -954,6 +956,7 @@ __device__ __forceinline__ void update_body(const KP &p)
         }
         if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
         const unsigned long long m = ranks_len<MR>(p, (int)((it + 1) % 3));
+        nnext = MR ? ~0u : (unsigned)m;
 #ifdef EIK_DIAG
         if (lead) {
             unsigned long long tnow;
@@ -1240,7 +1243,7 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
         }
         if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
         const unsigned m = vload(lenR);  // this rank's |R_r| (list length)
-        const unsigned long long mg = ranks_len<MR>(p, (int)(r % 3));  // global |R_r|
+        const unsigned long long mg = MR ? ranks_len<MR>(p, (int)(r % 3)) : m;  // global |R_r|
         if (lead) {
             ctl->iters = r + 1;
             ctl->sum += mg;
