@@ -1244,6 +1244,15 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
         if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
         const unsigned m = vload(lenR);  // this rank's |R_r| (list length)
         const unsigned long long mg = MR ? ranks_len<MR>(p, (int)(r % 3)) : m;  // global |R_r|
+        if (!p.slab && rr > p.it0) {
+            // R_r = D_{r-1} u (N(D_{r-1}) \ fixed) is empty exactly when round r-1 decreased
+            // nothing: the loop ends here (no separate read of |D_{r-1}| after its barrier)
+            if (mg == 0) break;
+            if (r >= (uint32_t)p.cap) {  // E/ifim.py:185-189
+                if (gb == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
+                break;
+            }
+        }
         if (lead) {
             ctl->iters = r + 1;
             ctl->sum += mg;
@@ -1331,14 +1340,11 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
             }
         }
         const unsigned long long td = block_sum(lane == 0 ? a_dec : 0ull, sred);
-        if (threadIdx.x == 0 && td) atomicAdd(&ctl->dsum[r % 3], td);
-        if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
-        unsigned long long decs = vload(&ctl->dsum[r % 3]);
-        if (MR) {
-            decs = 0;
-            for (int q = 0; q < p.R; ++q) decs += __ldcg(&p.rank_ctl[q]->dsum[r % 3]);
+        if (threadIdx.x == 0 && td) {
+            atomicAdd(&ctl->dsum[r % 3], td);
+            atomicAdd(&ctl->writes, td);
         }
-        if (p.slab) continue;  // the host reduces the counts and decides
+        if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
 #ifdef EIK_DIAG
         if (lead) {
             unsigned long long dgt2;
@@ -1346,12 +1352,8 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
             ctl->dg[2][dgb] += dgt2 - dgt1;
         }
 #endif
-        if (lead) ctl->writes += decs;
-        if (decs == 0) break;
-        if (r + 1 >= (uint32_t)p.cap) {  // E/ifim.py:185-189
-            if (gb == 0 && threadIdx.x == 0) ctl->err = EIK_ECAP;
-            break;
-        }
+        // slab mode: the host reduces the counts and decides; otherwise the next round's
+        // phase B finds R_{r+1} empty when D_r is
     }
 }
 
@@ -2668,7 +2670,7 @@ int eik_mr_run(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_be
     Ctl cu0, cr0;
     CK(cudaMemcpyAsync(&cu0, mu[0].kp.rank_ctl[0], sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(&cr0, mrm[0].kp.rank_ctl[0], sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-    unsigned long long writes = 0, conv = 0, freec = 0, flagged = 0;
+    unsigned long long writes = 0, conv = 0, freec = 0, flagged = 0, rwrites = 0;
     for (int r = 0; r < R; ++r) {
         Ctl cu, cr;
         CK(cudaMemcpyAsync(&cu, mu[0].kp.rank_ctl[r], sizeof(Ctl), cudaMemcpyDeviceToHost, st));
@@ -2679,6 +2681,7 @@ int eik_mr_run(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_be
         if (cu.err == EIK_ECAP) return fail(EIK_ECAP, "active list did not drain");
         if (cr.err == EIK_ECAP) return fail(EIK_ECAP, "remedy set did not drain");
         writes += cu.writes;
+        rwrites += cr.writes;
         conv += cu.conv;
         freec += cr.free_cells;
         flagged += cr.flagged;
@@ -2692,7 +2695,7 @@ int eik_mr_run(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_be
     out->peak_remedy = (int64_t)cr0.peak;
     out->iterations = out->upd_iterations + out->rem_iterations;
     out->solver_calls = out->upd_calls + out->build_calls + out->rem_calls;
-    out->phi_writes = (int64_t)(writes + cr0.writes);
+    out->phi_writes = (int64_t)(writes + rwrites);
     out->upd_ms = ev.ms(0, 1);
     out->build_ms = ev.ms(1, 2);
     out->rem_ms = ev.ms(2, 3);
