@@ -218,21 +218,31 @@ class Workspace:
 
 
 _WS: dict = {}
+_WS_LOCK = __import__("threading").Lock()
 
 
 def workspace(geom: _native.Geom, device: torch.device) -> Workspace:
-    key = (str(device), geom.nx, geom.ny, geom.nz, geom.ndim, geom.dtype)
-    ws = _WS.get(key)
-    if ws is None:
-        if len(_WS) >= 4:
-            _WS.clear()
-        ws = Workspace(geom, device)
-        _WS[key] = ws
+    """The calling thread's workspace for this geometry (kept between calls: the staged API
+    leaves the remedy set in it).  Per thread, so concurrent solves on different grids of the
+    same shape never share scratch memory (the reference's solvers are re-entrant)."""
+    import threading
+
+    key = (threading.get_ident(), str(device), geom.nx, geom.ny, geom.nz, geom.ndim, geom.dtype)
+    with _WS_LOCK:
+        ws = _WS.get(key)
+        if ws is None:
+            mine = [k for k in _WS if k[0] == key[0]]
+            if len(mine) >= 4:
+                for k in mine:
+                    del _WS[k]
+            ws = Workspace(geom, device)
+            _WS[key] = ws
     return ws
 
 
 def clear_workspaces() -> None:
-    _WS.clear()
+    with _WS_LOCK:
+        _WS.clear()
 
 
 def _ptr(t):

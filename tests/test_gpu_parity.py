@@ -339,3 +339,35 @@ def test_cfg2_full_size_properties():
     assert eik.field_max_diff(a.phi, b.phi) <= 1e-9
     assert eik.max_residual(g1) <= 1e-9
     assert a.stats.peak_remedy > 0 and a.stats.solver_calls > n * n
+
+
+def test_concurrent_solves_from_threads():
+    """Concurrent calls on different grids are allowed: two threads solving
+    same-shape grids at once get their own workspaces and the single-thread results."""
+    import threading
+
+    n = 48
+    k = np.arange(n) // 6
+    F1 = np.where(((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2) == 0, 1.0, 0.02)
+    F2 = np.exp(0.3 * np.sin(np.arange(n)[None, None, :] * 0.3) * np.ones((n, n, n)))
+    refs, outs, errs = [], [None, None], []
+    for F in (F1, F2):
+        g = eik.new_grid_3d(n, n, n, 1.0, speed=F)
+        refs.append(eik.solve_ifim(g, eik.seed_point(g, (5, 9, 13), 0.0)).phi)
+
+    def run(i, F):
+        try:
+            for _ in range(3):
+                g = eik.new_grid_3d(n, n, n, 1.0, speed=F)
+                outs[i] = eik.solve_ifim(g, eik.seed_point(g, (5, 9, 13), 0.0)).phi
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ts = [threading.Thread(target=run, args=(i, F)) for i, F in enumerate((F1, F2))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs
+    for o, r in zip(outs, refs):
+        assert np.array_equal(o.view(np.uint64), r.view(np.uint64))
