@@ -77,3 +77,26 @@ def test_random_problems_bit_exact(chunk):
         assert np.array_equal(np.asarray(fg.phi).view(np.uint64), fr.phi.view(np.uint64)), (shape, spacing)
         assert (fg.stats.iterations, fg.stats.solver_calls, fg.stats.peak_active) == (
             fr.stats["iterations"], fr.stats["solver_calls"], fr.stats["peak_active"])
+
+
+def test_random_3d_problems_peer_slabs():
+    """Random 3D problems through the multi-rank peer-slab kernels (R ranks emulated on one GPU)."""
+    from paper_2106_15869_b200.slab_peer import solve_emulated
+
+    rng = np.random.default_rng(77)
+    done = 0
+    while done < 12:
+        shape, spacing, F, seeds, vals = _problem(rng)
+        if len(shape) != 3 or shape[0] < 2:
+            continue
+        state = np.where(F == 0, 4, 0).astype(np.uint8)
+        R = int(rng.integers(1, min(shape[0], 6) + 1))
+        ref = cpu.solve_ifim(shape, spacing, F, seeds, vals, state=state, threads=1)
+        dev = torch.device("cuda:0")
+        phi, st, state_out = solve_emulated(shape, spacing, torch.as_tensor(F, device=dev),
+                                            torch.as_tensor(state, device=dev), list(zip(seeds, vals)), R)
+        assert np.array_equal(phi.cpu().numpy().view(np.uint64), ref.phi.view(np.uint64)), (shape, R)
+        assert (st.solver_calls, st.iterations, st.peak_remedy) == (
+            ref.stats["solver_calls"], ref.stats["iterations"], ref.stats["peak_remedy"]), (shape, R)
+        assert st.active_history == ref.active_history
+        done += 1
