@@ -646,7 +646,7 @@ def main():
     ap.add_argument("--size", type=int, default=None, help="grid edge (default 512; cfg5: 1024)")
     ap.add_argument("--config", default="cfg4", choices=["cfg3", "cfg4", "cfg5"],
                     help="BASELINE.json config (cfg4 = the headline 512^3 checkerboard)")
-    ap.add_argument("--cpu-size", type=int, default=96)
+    ap.add_argument("--cpu-size", type=int, default=144, help="edge of the bounded CPU sample (~10-15 s of oracle work)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
