@@ -121,11 +121,6 @@ def make_workload(torch, dev, config, n):
     return Workload("cfg4", n, 1.0, F, [(c, c, c)], workload_desc(config, n))
 
 
-def checker_speed_np(n: int, blk: int) -> np.ndarray:
-    k = np.arange(n) // blk
-    return np.where(((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2) == 0, 1.0, 0.01)
-
-
 def hbm_peak():
     try:
         with open(PEAKS_FILE) as fh:
