@@ -13,6 +13,13 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
+    # a fresh checkout has no built libraries (*.so are not tracked): build them once (mtime
+    # based, a no-op when current; nvcc cross-compiles sm_100a without a GPU)
+    from oracle import cpu
+    from paper_2106_15869_b200 import _native
+
+    _native.build()
+    cpu.build()
     config.addinivalue_line("markers", "slow: full BASELINE-size cases")
 
 
