@@ -576,6 +576,7 @@ def run_ours(args):
                        "l2": f"inputs larger than L2 (phi {n ** 3 * 8 / 2 ** 30:g} GiB fp64 per field at {n}^3)",
                        "phase_ms": r.phase_ms},
             "wall_clock_to_convergence_ms": ms / args.steps,
+            "grid_cells_per_s": n ** 3 / (ms / args.steps * 1e-3),  # N / wall
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "k_fim" if args.method == "fim" else "k_remedy", "alg_bytes_per_launch": alg_bytes,
