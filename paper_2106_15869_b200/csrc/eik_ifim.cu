@@ -993,6 +993,9 @@ __device__ __forceinline__ void update_body(const KP &p)
     }
 }
 
+#ifndef UPD_2D_PER_SM
+#define UPD_2D_PER_SM 1  // update step CTAs per SM on 2D grids (thin O(n) fronts)
+#endif
 #ifndef UPD_MINB
 #define UPD_MINB 3  // update step: CTAs per SM the register budget is sized for
 #endif
@@ -1931,7 +1934,7 @@ struct Engine {
     {
         // 2D fronts are O(n) cells: one CTA per SM keeps the per-iteration barrier cheap
         // (cfg2 4096^2: 29 vs 34 ms); 3D fronts are O(n^2) and want the full occupancy
-        return coop_launch(k_update<DIM, SOL>, p, nullptr, false, st, "EIK_UPD_BLOCKS_PER_SM", DIM == 2 ? 1 : 0);
+        return coop_launch(k_update<DIM, SOL>, p, nullptr, false, st, "EIK_UPD_BLOCKS_PER_SM", DIM == 2 ? UPD_2D_PER_SM : 0);
     }
     // remedy-set slots: counters (R0 is rewritten word by word)
     static int reset_set(KP &p, cudaStream_t st)
