@@ -47,14 +47,33 @@ UNIT = "node-updates/s"
 
 
 class Workload:
-    """One BASELINE.json config: speed field (device tensor), spacing, point seeds (i, j, k)."""
+    """One BASELINE.json config: speed field (device tensor), spacing, point seeds ((i, j) or
+    (i, j, k)); 2D configs are n^2, 3D configs n^3."""
 
     def __init__(self, name, n, h, F, seeds, desc):
         self.name, self.n, self.h, self.F, self.seeds, self.desc = name, n, h, F, seeds, desc
+        self.ndim = F.dim()
+        self.shape = tuple(F.shape)
+        self.cells = int(np.prod(self.shape))
 
     def linear_seeds(self):
         n = self.n
+        if self.ndim == 2:
+            return [(j * n + i, 0.0) for i, j in self.seeds]
         return [((k * n + j) * n + i, 0.0) for i, j, k in self.seeds]
+
+    def spacing(self):
+        return (self.h, self.h) if self.ndim == 2 else self.h
+
+    def grid(self, eik, phi, F, state):
+        n = self.n
+        if self.ndim == 2:
+            return eik.Grid(n, n, self.h, self.h, (0.0, 0.0), phi, F, state)
+        return eik.Grid3D(n, n, n, self.h, (0.0, 0.0, 0.0), phi, F, state)
+
+    def bc(self, eik):
+        idx = eik.CellIndex if self.ndim == 2 else eik.CellIndex3D
+        return eik.BoundaryCondition(tuple((idx(*s), 0.0) for s in self.seeds))
 
 
 def cfg5_modes(n):
@@ -93,6 +112,10 @@ def cfg5_speed(torch, dev, n):
 
 
 def workload_desc(config, n):
+    if config == "cfg1":
+        return f"cfg1: 2D {n}^2 F=1, h=1, centre seed"
+    if config == "cfg2":
+        return f"cfg2: 2D {n}^2 on [0,1]^2, F=1+0.5 sin(2 pi x) sin(2 pi y), 8 seeds (rng 2106)"
     if config == "cfg5":
         return f"cfg5: 3D {n}^3 on [0,1]^3, F=exp(0.5 g) (32 Fourier modes |k|<=4, rng 2106), 16 seeds"
     if config == "cfg3":
@@ -101,6 +124,20 @@ def workload_desc(config, n):
 
 
 def make_workload(torch, dev, config, n):
+    if config == "cfg1":
+        return Workload("cfg1", n, 1.0, torch.ones((n, n), dtype=torch.float64, device=dev), [(n // 2, n // 2)],
+                        workload_desc(config, n))
+    if config == "cfg2":
+        h = 1.0 / (n - 1)
+        x = torch.arange(n, dtype=torch.float64, device=dev) * h
+        F = 1 + 0.5 * torch.sin(2 * np.pi * x)[None, :] * torch.sin(2 * np.pi * x)[:, None]
+        rng = np.random.default_rng(2106)
+        seeds = []
+        while len(seeds) < 8:
+            c = tuple(int(v) for v in rng.integers(0, n, 2))
+            if c not in seeds:
+                seeds.append(c)
+        return Workload("cfg2", n, h, F, seeds, workload_desc(config, n))
     if config == "cfg5":
         F, h, seeds = cfg5_speed(torch, dev, n)
         return Workload("cfg5", n, h, F, seeds, workload_desc(config, n))
@@ -213,7 +250,7 @@ def cpu_sample(n: int, threads: int, config: str = "cfg4"):
     F = w.F.numpy()
     sd = w.linear_seeds()
     t0 = time.perf_counter()
-    res = cpu.solve_ifim((n, n, n), w.h, F, [c for c, _ in sd], [v for _, v in sd], threads=threads)
+    res = cpu.solve_ifim(w.shape, w.spacing(), F, [c for c, _ in sd], [v for _, v in sd], threads=threads)
     dt = time.perf_counter() - t0
     return res.stats["solver_calls"], dt
 
@@ -264,12 +301,12 @@ class StepStats:
 def make_fim_step(eik, torch, dev, w, dtype):
     """One device-resident solve_fim (the paper's FIM baseline, E/fim.py) of the whole grid.
     Its whole persistent kernel stands in for the roofline kernel: bytes = 8 x (2 calls + writes)."""
-    n, F = w.n, w.F.to(dtype)
-    phi0 = torch.full((n, n, n), float("inf"), dtype=dtype, device=dev)
-    st0 = torch.zeros((n, n, n), dtype=torch.uint8, device=dev)
+    F = w.F.to(dtype)
+    phi0 = torch.full(w.shape, float("inf"), dtype=dtype, device=dev)
+    st0 = torch.zeros(w.shape, dtype=torch.uint8, device=dev)
     phi, st = torch.empty_like(phi0), torch.empty_like(st0)
-    g = eik.Grid3D(n, n, n, w.h, (0.0, 0.0, 0.0), phi, F, st)
-    bc = eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in w.seeds))
+    g = w.grid(eik, phi, F, st)
+    bc = w.bc(eik)
 
     def step():
         phi.copy_(phi0)
@@ -283,12 +320,12 @@ def make_fim_step(eik, torch, dev, w, dtype):
 
 def make_single_step(eik, torch, dev, w, dtype):
     """One device-resident solve_ifim of the whole grid (inputs restored in the step)."""
-    n, F = w.n, w.F.to(dtype)
-    phi0 = torch.full((n, n, n), float("inf"), dtype=dtype, device=dev)
-    st0 = torch.zeros((n, n, n), dtype=torch.uint8, device=dev)
+    F = w.F.to(dtype)
+    phi0 = torch.full(w.shape, float("inf"), dtype=dtype, device=dev)
+    st0 = torch.zeros(w.shape, dtype=torch.uint8, device=dev)
     phi, st = torch.empty_like(phi0), torch.empty_like(st0)
-    g = eik.Grid3D(n, n, n, w.h, (0.0, 0.0, 0.0), phi, F, st)
-    bc = eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in w.seeds))
+    g = w.grid(eik, phi, F, st)
+    bc = w.bc(eik)
 
     def step():
         phi.copy_(phi0)
@@ -473,8 +510,8 @@ def run_ours(args):
     workload = w.desc
     rdt = torch.float32 if args.dtype == "f32" else torch.float64
     rsize = 4 if args.dtype == "f32" else 8
-    if (args.dtype == "f32" or args.method == "fim") and (world > 1 or args.slabs):
-        raise SystemExit("the float32 perf mode and the FIM baseline are single-device")
+    if (args.dtype == "f32" or args.method == "fim" or w.ndim == 2) and (world > 1 or args.slabs):
+        raise SystemExit("the float32 perf mode, the FIM baseline and the 2D configs are single-device")
     slabs = world > 1 or args.slabs
     mode = "single"
     if world > 1 and not args.host_slabs and peer_slabs_possible(torch, dev, world, local):
@@ -573,10 +610,11 @@ def run_ours(args):
                        "iterations": r.iterations, "peak_remedy": r.peak_remedy,
                        "parallelism": {"peer": f"z-slabs x{world} (peer-memory fused kernels)",
                                        "host": f"z-slabs x{world} (host-driven exchange)"}.get(mode, "single"),
-                       "l2": f"inputs larger than L2 (phi {n ** 3 * 8 / 2 ** 30:g} GiB fp64 per field at {n}^3)",
+                       "l2": (f"inputs larger than L2 (phi {w.cells * 8 / 2 ** 30:g} GiB fp64 per field)"
+                              if w.cells * 8 > (126 << 20) else "inputs smaller than L2 (cfg1/cfg2-size 2D grid)"),
                        "phase_ms": r.phase_ms},
             "wall_clock_to_convergence_ms": ms / args.steps,
-            "grid_cells_per_s": n ** 3 / (ms / args.steps * 1e-3),  # N / wall
+            "grid_cells_per_s": w.cells / (ms / args.steps * 1e-3),  # N / wall
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "k_fim" if args.method == "fim" else "k_remedy", "alg_bytes_per_launch": alg_bytes,
@@ -606,11 +644,10 @@ def run_ours(args):
 def run_e2e(eik, torch, dev, w, calls, args, rdt):
     """Same metric through solve_ifim with host buffers: H2D of phi/speed/state from pinned
     memory and D2H of phi inside each timed step."""
-    n = w.n
     speed = w.F.to(rdt).cpu().pin_memory()
-    phi = torch.empty((n, n, n), dtype=rdt).pin_memory()
-    state = torch.empty((n, n, n), dtype=torch.uint8).pin_memory()
-    bc = eik.BoundaryCondition(tuple((eik.CellIndex3D(*s), 0.0) for s in w.seeds))
+    phi = torch.empty(w.shape, dtype=rdt).pin_memory()
+    state = torch.empty(w.shape, dtype=torch.uint8).pin_memory()
+    bc = w.bc(eik)
     steps = max(1, min(args.steps, 3))
     warm = 2  # allocations: device grid, workspace, pinned result copies (cached by torch afterwards)
     tot = 0.0
@@ -618,7 +655,7 @@ def run_e2e(eik, torch, dev, w, calls, args, rdt):
     for it in range(steps + warm):
         phi.fill_(float("inf"))
         state.zero_()
-        g = eik.Grid3D(n, n, n, w.h, (0.0, 0.0, 0.0), phi, speed, state)
+        g = w.grid(eik, phi, speed, state)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         res = eik.solve_ifim(g, bc)
@@ -626,7 +663,7 @@ def run_e2e(eik, torch, dev, w, calls, args, rdt):
         assert res.stats.solver_calls == calls
         if it >= warm:
             tot += dt
-    N = n ** 3
+    N = w.cells
     # D2H: phi into the caller's array (in-place API) and into SolverResult.phi (the
     # reference returns grid.phi.copy()), both DMA from the device
     rs = phi.element_size()
@@ -640,7 +677,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--size", type=int, default=None, help="grid edge (default 512; cfg5: 1024)")
-    ap.add_argument("--config", default="cfg4", choices=["cfg3", "cfg4", "cfg5"],
+    ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="BASELINE.json config (cfg4 = the headline 512^3 checkerboard)")
     ap.add_argument("--cpu-size", type=int, default=144, help="edge of the bounded CPU sample (~10-15 s of oracle work)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -654,7 +691,7 @@ def main():
     ap.add_argument("--host-slabs", action="store_true", help="N>1: host-driven NCCL slabs instead of peer memory")
     args = ap.parse_args()
     if args.size is None:
-        args.size = 1024 if args.config == "cfg5" else (256 if args.config == "cfg3" else 512)
+        args.size = {"cfg1": 256, "cfg2": 4096, "cfg3": 256, "cfg5": 1024}.get(args.config, 512)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
