@@ -123,39 +123,75 @@ def workload_desc(config, n):
     return f"cfg4: 3D {n}^3 checkerboard 1:100 ({max(1, n // 16)}^3 blocks), h=1, seed (c,c,c)"
 
 
-def make_workload(torch, dev, config, n):
+def _distinct_cells(rng, n, k, dim):
+    out = []
+    while len(out) < k:
+        c = tuple(int(v) for v in rng.integers(0, n, dim))
+        if c not in out:
+            out.append(c)
+    return out
+
+
+def cfg5_speed_np(n):
+    """cfg5's F = exp(0.5 g) on the host (numpy, plane chunks on a thread pool: the ufuncs
+    release the GIL), same expression order as cfg5_speed."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    K, ph, seeds = cfg5_modes(n)
+    h = 1.0 / (n - 1)
+    x = np.arange(n, dtype=np.float64) * h
+    F = np.empty((n, n, n), dtype=np.float64)
+    zc = max(1, (1 << 21) // (n * n))
+
+    def chunk(z0):
+        z1 = min(n, z0 + zc)
+        g = np.zeros((z1 - z0, n, n), dtype=np.float64)
+        for (kx, ky, kz), p in zip(K.tolist(), ph.tolist()):
+            a = 2 * np.pi * (kz * x[z0:z1])[:, None, None] + (2 * np.pi * ky * x)[None, :, None] + \
+                (2 * np.pi * kx * x + p)[None, None, :]
+            g += np.cos(a)
+        F[z0:z1] = np.exp(0.5 * 0.25 * g)
+
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 1) as ex:
+        list(ex.map(chunk, range(0, n, zc)))
+    return F, h, seeds
+
+
+# cfg5 fields up to this edge are built on the host with numpy (bit-identical to the field the
+# full-size oracle digests in tests/golden/fullsize.json were computed on); larger ones on the
+# device with torch (CUDA cos/exp may differ from numpy's in the last bit)
+CFG5_HOST_MAX = 512
+
+
+def workload_np(config, n):
+    """(h, F, seeds) of one BASELINE.json config built on the host with numpy.  Every field here
+    is bit-identical to what the oracle digests (tests/golden/make_fullsize.py) used."""
     if config == "cfg1":
-        return Workload("cfg1", n, 1.0, torch.ones((n, n), dtype=torch.float64, device=dev), [(n // 2, n // 2)],
-                        workload_desc(config, n))
+        return 1.0, np.ones((n, n)), [(n // 2, n // 2)]
     if config == "cfg2":
         h = 1.0 / (n - 1)
-        x = torch.arange(n, dtype=torch.float64, device=dev) * h
-        F = 1 + 0.5 * torch.sin(2 * np.pi * x)[None, :] * torch.sin(2 * np.pi * x)[:, None]
-        rng = np.random.default_rng(2106)
-        seeds = []
-        while len(seeds) < 8:
-            c = tuple(int(v) for v in rng.integers(0, n, 2))
-            if c not in seeds:
-                seeds.append(c)
-        return Workload("cfg2", n, h, F, seeds, workload_desc(config, n))
+        x = np.arange(n, dtype=np.float64) * h
+        F = 1 + 0.5 * np.sin(2 * np.pi * x)[None, :] * np.sin(2 * np.pi * x)[:, None]
+        return h, F, _distinct_cells(np.random.default_rng(2106), n, 8, 2)
+    if config == "cfg3":
+        return 1.0, np.ones((n, n, n)), _distinct_cells(np.random.default_rng(2106), n, 16, 3)
     if config == "cfg5":
+        F, h, seeds = cfg5_speed_np(n)
+        return h, F, seeds
+    blk = max(1, n // 16)
+    kk = np.arange(n) // blk
+    F = np.where(((kk[:, None, None] + kk[None, :, None] + kk[None, None, :]) % 2) == 0, 1.0, 0.01)
+    c = n // 2
+    return 1.0, F, [(c, c, c)]
+
+
+def make_workload(torch, dev, config, n):
+    if config == "cfg5" and n > CFG5_HOST_MAX:
         F, h, seeds = cfg5_speed(torch, dev, n)
         return Workload("cfg5", n, h, F, seeds, workload_desc(config, n))
-    if config == "cfg3":
-        rng = np.random.default_rng(2106)
-        seeds = []
-        while len(seeds) < 16:
-            s = tuple(int(v) for v in rng.integers(0, n, 3))
-            if s not in seeds:
-                seeds.append(s)
-        return Workload("cfg3", n, 1.0, torch.ones((n, n, n), dtype=torch.float64, device=dev), seeds,
-                        workload_desc(config, n))
-    blk = max(1, n // 16)
-    kk = torch.arange(n, device=dev) // blk
-    one, slow = torch.tensor(1.0, dtype=torch.float64), torch.tensor(0.01, dtype=torch.float64)  # exact 1:100
-    F = torch.where(((kk[:, None, None] + kk[None, :, None] + kk[None, None, :]) % 2) == 0, one, slow)
-    c = n // 2
-    return Workload("cfg4", n, 1.0, F, [(c, c, c)], workload_desc(config, n))
+    h, F, seeds = workload_np(config, n)
+    return Workload(config, n, h, torch.from_numpy(np.ascontiguousarray(F)).to(dev), seeds,
+                    workload_desc(config, n))
 
 
 def hbm_peak():
@@ -337,6 +373,7 @@ def make_single_step(eik, torch, dev, w, dtype):
         rem_writes = s.phi_writes - upd_writes
         st_ = StepStats(s.solver_calls, s.iterations, s.peak_remedy, ph["remedy"]["solver_calls"], rem_writes,
                         s.device_ms["remedy"], s.gpu_launches, {k: round(v, 3) for k, v in s.device_ms.items()})
+        st_.run_stats, st_.phi = s, phi
         # per-phase algorithmic bytes (8 B x (2 calls + writes); build: 2 x 8 B per free cell)
         rs = phi.element_size()
         st_.phase_bytes = {"update": rs * (2 * ph["update"]["solver_calls"] + upd_writes),
@@ -435,14 +472,16 @@ def make_peer_step(torch, dev, w, world, rank):
 
     def step():
         st.copy_(st0)
-        _, s = ds.solve(sp, st, seeds)
+        phi_l, s = ds.solve(sp, st, seeds)
         ph = s.phases
         upd_writes = ph["update"]["solver_calls"] - ph["update"]["converged"]
         rem_writes = s.phi_writes - upd_writes
         st_ = StepStats(s.solver_calls, s.iterations, s.peak_remedy, ph["remedy"]["solver_calls"], rem_writes,
                         s.device_ms["remedy"], s.gpu_launches, {k: round(v, 3) for k, v in s.device_ms.items()})
-        # per-phase algorithmic bytes (8 B x (2 calls + writes); build: 2 x 8 B per free cell)
-        rs = phi.element_size()
+        st_.run_stats, st_.phi = s, phi_l
+        # per-phase algorithmic bytes (8 B x (2 calls + writes); build: 2 x 8 B per free cell);
+        # the peer-slab engine is float64
+        rs = 8
         st_.phase_bytes = {"update": rs * (2 * ph["update"]["solver_calls"] + upd_writes),
                            "build": rs * 2 * ph["build"]["solver_calls"],
                            "remedy": rs * (2 * ph["remedy"]["solver_calls"] + rem_writes)}
@@ -491,6 +530,71 @@ def run_e2e_peer(torch, dev, w, world, rank, calls, args):
             "note": "per rank (rank 0's slab); wall time max over ranks"}
 
 
+FULLSIZE = os.path.join(ROOT, "tests", "golden", "fullsize.json")
+
+
+def parity_vs_oracle(torch, w, r, world, rank, dtype):
+    """After the timed steps: the last solve's phi sha256 and every RunStats integer against the
+    full-size oracle digests (tests/golden/fullsize.json, made by tests/golden/make_fullsize.py
+    from oracle/eik_oracle.c, which is pinned to the live reference).  Peer slabs: rank 0 hashes
+    the slabs in z order (received over the process group).  Returns (status, detail)."""
+    import hashlib
+
+    if dtype != "f64":
+        return "not-applicable", "float32 perf mode (checked against float64 at max-rel 1e-5 in tests)"
+    s = getattr(r, "run_stats", None)
+    if s is None:
+        return "not-checked", "host-driven slab protocol"
+    try:
+        with open(FULLSIZE) as fh:
+            rec = json.load(fh).get(f"{w.name}@{w.n}")
+    except OSError:
+        rec = None
+    if rec is None:
+        return "unpinned", f"no full-size oracle digest for {w.name}@{w.n}"
+    h = hashlib.sha256()
+    if world > 1:
+        import torch.distributed as dist
+
+        if rank == 0:
+            h.update(r.phi.cpu().numpy().tobytes())
+            for src in range(1, world):
+                n = torch.zeros(1, dtype=torch.int64, device=r.phi.device)
+                dist.recv(n, src)
+                buf = torch.empty(int(n.item()), dtype=torch.float64, device=r.phi.device)
+                dist.recv(buf, src)
+                h.update(buf.cpu().numpy().tobytes())
+        else:
+            dist.send(torch.tensor([r.phi.numel()], dtype=torch.int64, device=r.phi.device), 0)
+            dist.send(r.phi.reshape(-1).contiguous(), 0)
+            return None, None
+        speed_ok = True  # each rank's slab of the same host-built field
+    else:
+        h.update(r.phi.cpu().numpy().tobytes())
+        speed_ok = hashlib.sha256(w.F.cpu().numpy().tobytes()).hexdigest() == rec["speed_sha256"]
+    ph = s.phases
+    got = {"iterations": s.iterations, "solver_calls": s.solver_calls, "peak_active": s.peak_active,
+           "peak_remedy": s.peak_remedy, "phi_writes": s.phi_writes,
+           "upd_iterations": ph["update"]["iterations"], "upd_calls": ph["update"]["solver_calls"],
+           "frozen": ph["update"]["converged"], "build_calls": ph["build"]["solver_calls"],
+           "remedy_size": ph["build"]["remedy_size"], "rem_iterations": ph["remedy"]["iterations"],
+           "rem_calls": ph["remedy"]["solver_calls"],
+           "active_history_sha256": hashlib.sha256(np.asarray(s.active_history, dtype=np.int64).tobytes()).hexdigest(),
+           "phi_sha256": h.hexdigest()}
+    u, b, m = rec["update"], rec["build"], rec["remedy"]
+    want = {**{k: rec["stats"][k] for k in ("iterations", "solver_calls", "peak_active", "peak_remedy", "phi_writes")},
+            "upd_iterations": u["iterations"], "upd_calls": u["solver_calls"], "frozen": u["frozen"],
+            "build_calls": b["calls"], "remedy_size": b["remedy_size"], "rem_iterations": m["iterations"],
+            "rem_calls": m["solver_calls"], "active_history_sha256": u["active_history_sha256"],
+            "phi_sha256": rec["phi_sha256"]}
+    bad = [k for k in want if got[k] != want[k]]
+    if not speed_ok:
+        return "unpinned", "speed field differs from the digested one"
+    if bad:
+        return "mismatch", "; ".join(f"{k}: {got[k]} != {want[k]}" for k in bad)
+    return "digest-match", f"phi sha256 + {len(want) - 1} RunStats fields equal the oracle's ({w.name}@{w.n})"
+
+
 def run_ours(args):
     import torch
 
@@ -499,7 +603,7 @@ def run_ours(args):
         raise SystemExit("bench.py needs a CUDA device")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if world > 1 or args.force_peer:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=dev)
@@ -512,26 +616,20 @@ def run_ours(args):
     rsize = 4 if args.dtype == "f32" else 8
     if (args.dtype == "f32" or args.method == "fim" or w.ndim == 2) and (world > 1 or args.slabs):
         raise SystemExit("the float32 perf mode, the FIM baseline and the 2D configs are single-device")
-    slabs = world > 1 or args.slabs
+    slabs = world > 1 or args.slabs or args.force_peer
     mode = "single"
-    if world > 1 and not args.host_slabs and peer_slabs_possible(torch, dev, world, local):
+    if (world > 1 or args.force_peer) and not args.host_slabs:
+        # the fused peer-memory kernels; any failure is fatal (--host-slabs selects the NCCL protocol)
         import torch.distributed as dist
 
-        try:  # symmetric-memory slabs, a verified small solve and one probe solve; any rank failing
-            # sends every rank to the NCCL path
-            ok = int(peer_slabs_verify(torch, dev, world, rank))
-            if not ok:
-                print(f"[bench] peer-memory slabs disagree with the single-device solve on rank {rank}",
-                      file=sys.stderr, flush=True)
-            step, mode = make_peer_step(torch, dev, w, world, rank), "peer"
-            step()
-        except Exception as e:  # noqa: BLE001
-            print(f"[bench] peer-memory slabs unavailable on rank {rank}: {e!r}", file=sys.stderr, flush=True)
-            ok = 0
-        t = torch.tensor([ok], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MIN)
-        if not t.item():
-            step, mode = make_slab_step(torch, dev, w, world, rank), "host"
+        if not peer_slabs_possible(torch, dev, world, local):
+            raise SystemExit("peer-memory slabs need P2P mappings between every pair of ranks' GPUs; "
+                             "pass --host-slabs for the host-driven NCCL protocol")
+        ok = torch.tensor([int(peer_slabs_verify(torch, dev, world, rank))], device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not ok.item():
+            raise SystemExit("peer-memory slabs disagree with the single-device solve (small verification grid)")
+        step, mode = make_peer_step(torch, dev, w, world, rank), "peer"
     elif slabs:
         step, mode = make_slab_step(torch, dev, w, world, rank), "host"
     elif args.method == "fim":
@@ -584,6 +682,8 @@ def run_ours(args):
     achieved = alg_bytes / rem_s / 1e9 if rem_s > 0 else None
     traffic = traffic_from_profiles(workload) if not slabs and args.dtype == "f64" and args.method == "ifim" else None
 
+    parity, parity_detail = parity_vs_oracle(torch, w, r, world, rank, args.dtype) if args.method == "ifim" \
+        else ("not-checked", "FIM baseline (bit-exact vs the oracle in tests/test_gpu_fim.py)")
     out = None
     e2e_peer = None
     if mode == "peer" and not args.no_e2e:  # collective: every rank takes part
@@ -613,6 +713,7 @@ def run_ours(args):
                        "l2": (f"inputs larger than L2 (phi {w.cells * 8 / 2 ** 30:g} GiB fp64 per field)"
                               if w.cells * 8 > (126 << 20) else "inputs smaller than L2 (cfg1/cfg2-size 2D grid)"),
                        "phase_ms": r.phase_ms},
+            "parity": parity, "parity_detail": parity_detail,
             "wall_clock_to_convergence_ms": ms / args.steps,
             "grid_cells_per_s": w.cells / (ms / args.steps * 1e-3),  # N / wall
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -631,13 +732,16 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clocks,
         }
-    if world > 1:
+    if world > 1 or args.force_peer:
         import torch.distributed as dist
 
         dist.barrier()
         dist.destroy_process_group()
     if out is not None:
         print(json.dumps(out), flush=True)
+        if out["parity"] == "mismatch":
+            print(f"[bench] RESULT MISMATCH vs the oracle digests: {out['parity_detail']}", file=sys.stderr, flush=True)
+            return 3
     return 0
 
 
@@ -689,6 +793,8 @@ def main():
                     help="f64 = parity mode (default, bit-exact); f32 = perf mode (max-rel 1e-5)")
     ap.add_argument("--slabs", action="store_true", help="use the z-slab protocol even on one GPU")
     ap.add_argument("--host-slabs", action="store_true", help="N>1: host-driven NCCL slabs instead of peer memory")
+    ap.add_argument("--force-peer", action="store_true",
+                    help="run the peer-memory slab kernels even at N=1 (under torchrun; a test of that path)")
     args = ap.parse_args()
     if args.size is None:
         args.size = {"cfg1": 256, "cfg2": 4096, "cfg3": 256, "cfg5": 1024}.get(args.config, 512)

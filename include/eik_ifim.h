@@ -93,6 +93,12 @@ int eik_build_remedy(const eik_geom *g, const double *phi, const double *speed, 
 int eik_remedy_load(const eik_geom *g, const uint8_t *member, const uint8_t *state, void *workspace,
                     size_t workspace_bytes, int64_t *count, void *stream);
 
+/* Load a hand-built RemedySet (E/ifim.py:64-72): `cells` marks its work list (the cells the first
+ * round relaxes), `member` its membership mask (NULL: equal to cells).  Members outside the work
+ * list are never relaxed and never enqueued (E/ifim.py:184-213).  *count = |work list|. */
+int eik_remedy_load_set(const eik_geom *g, const uint8_t *cells, const uint8_t *member, const uint8_t *state,
+                        void *workspace, size_t workspace_bytes, int64_t *count, void *stream);
+
 /* Write the workspace remedy set as a device uint8 mask[N]. */
 int eik_remedy_export(const eik_geom *g, void *workspace, size_t workspace_bytes, uint8_t *member,
                       void *stream);
@@ -207,6 +213,8 @@ int eik_build_remedy_f32(const eik_geom *g, const float *phi, const float *speed
                          void *workspace, size_t workspace_bytes, eik_stats *out, void *stream);
 int eik_remedy_load_f32(const eik_geom *g, const uint8_t *member, const uint8_t *state, void *workspace,
                         size_t workspace_bytes, int64_t *count, void *stream);
+int eik_remedy_load_set_f32(const eik_geom *g, const uint8_t *cells, const uint8_t *member, const uint8_t *state,
+                            void *workspace, size_t workspace_bytes, int64_t *count, void *stream);
 int eik_remedy_export_f32(const eik_geom *g, void *workspace, size_t workspace_bytes, uint8_t *member, void *stream);
 int eik_remedy_step_f32(const eik_geom *g, float *phi, const float *speed, const uint8_t *state, double tol,
                         void *workspace, size_t workspace_bytes, eik_stats *out, void *stream);

@@ -30,7 +30,7 @@ NVCC_FLAGS = [
 ]
 
 EXPORTS = (
-    "eik_workspace_size", "eik_ifim_update_step", "eik_build_remedy", "eik_remedy_load",
+    "eik_workspace_size", "eik_ifim_update_step", "eik_build_remedy", "eik_remedy_load", "eik_remedy_load_set",
     "eik_remedy_export", "eik_remedy_step", "eik_ifim_solve", "eik_local_solve",
     "eik_last_error", "eik_version", "eik_workspace_offsets", "eik_slab_update_init", "eik_slab_update_iter",
     "eik_slab_apply_requests", "eik_slab_build", "eik_slab_remedy_round", "eik_solve_fixpoint",
@@ -90,6 +90,7 @@ class Stats(C.Structure):
 
 EXPORTS_F32 = (
     "eik_workspace_size_f32", "eik_ifim_update_step_f32", "eik_build_remedy_f32", "eik_remedy_load_f32",
+    "eik_remedy_load_set_f32",
     "eik_remedy_export_f32", "eik_remedy_step_f32", "eik_ifim_solve_f32", "eik_solve_fixpoint_f32",
     "eik_max_residual_f32", "eik_local_solve_f32", "eik_last_error_f32", "eik_version_f32", "eik_solve_fim_f32",
 )
@@ -128,6 +129,7 @@ def lib(dtype: int = EIK_F64):
     L.eik_ifim_update_step.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]
     L.eik_build_remedy.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, SP, vp]
     L.eik_remedy_load.argtypes = [GP, P, P, P, C.c_size_t, C.POINTER(i64), vp]
+    L.eik_remedy_load_set.argtypes = [GP, P, P, P, P, C.c_size_t, C.POINTER(i64), vp]
     L.eik_remedy_export.argtypes = [GP, P, C.c_size_t, P, vp]
     L.eik_remedy_step.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, SP, vp]
     L.eik_ifim_solve.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]
@@ -164,6 +166,7 @@ def _lib_f32():
     L.eik_ifim_update_step_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]
     L.eik_build_remedy_f32.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, SP, vp]
     L.eik_remedy_load_f32.argtypes = [GP, P, P, P, C.c_size_t, C.POINTER(i64), vp]
+    L.eik_remedy_load_set_f32.argtypes = [GP, P, P, P, P, C.c_size_t, C.POINTER(i64), vp]
     L.eik_remedy_export_f32.argtypes = [GP, P, C.c_size_t, P, vp]
     L.eik_remedy_step_f32.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, SP, vp]
     L.eik_ifim_solve_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]

@@ -108,6 +108,7 @@ struct Ctl {
     unsigned long long dsum[3];     // remedy: |D_r| per rotating slot
     unsigned long long nz_words;    // remedy diagnostics: non-empty member words / 4-cell sectors
     unsigned long long nz_sectors;
+    unsigned stale;                 // remedy: a hand-built set has members outside its work list (St)
     unsigned wcount;                // multi-rank: world-barrier arrivals (rank 0's copy is used)
     unsigned wgen;                  // multi-rank: this rank's world-barrier generation
     unsigned fc[3];                 // FIM: check-list length per rotating slot
@@ -184,6 +185,15 @@ struct KP {
     uint32_t *R0b;       // R_0 (build / load)
     uint32_t *D0b, *D1b;  // D_r (decreased cells), double-buffered by round parity
     uint32_t *Fb;        // fixed = blocked | source | outside the row
+    // remedy tile engine (k_remedy_t, single device): tile-major bitmaps (one 128-byte line of 32
+    // row words per tile), per-tile D stamps by round parity, sharded chunk counters
+    uint32_t nty, ntz, ntiles, rt_shs;  // tiles in y / z, tiles, tiles per shard
+    FastDiv fnty;
+    uint32_t *Ft;                // fixed, tile-major (rows outside the grid: all fixed)
+    uint32_t *St;                // hand-built sets: members outside the work list, tile-major
+    uint32_t *Dt0, *Dt1;         // D_r, tile-major, by round parity
+    uint32_t *stamp0, *stamp1;   // per tile: (round + 1) << 7 | faces of its D_r line, by round parity
+    unsigned *grab;              // [3 slots][RT_SHARDS] chunk counters, one 128-byte line each
     // multi-rank (peer slabs): this rank owns planes [zg0, zg0 + nz) of the global grid
     int32_t mr, q, R, pad2;
     uint32_t gb0, gnb;     // this rank's CTAs: blockIdx.x in [gb0, gb0 + gnb)
@@ -192,6 +202,33 @@ struct KP {
 };
 
 
+
+// Remedy tile engine geometry (k_remedy_t below)
+#ifndef REMEDY_TILE_DEFAULT
+#define REMEDY_TILE_DEFAULT 0  // single-device remedy: 1 = tile engine, 0 = member-list kernel
+#endif
+#ifndef RT_SHARDS
+#define RT_SHARDS 32
+#endif
+#ifndef RT_CHUNK
+#define RT_CHUNK 4  // tiles per grab (<= 4: 7 stamp lanes per tile)
+#endif
+#ifndef RT_MINB
+#define RT_MINB 4
+#endif
+constexpr int RT_GS = 32;  // grab counter stride (uint32): one 128-byte line per shard and slot
+enum { FS_SELF = 1, FS_XL = 2, FS_XH = 4, FS_YL = 8, FS_YH = 16, FS_ZL = 32, FS_ZH = 64 };
+
+template <int DIM>
+struct TileGeo {
+    static constexpr int LY = DIM == 3 ? 3 : 5, LZ = DIM == 3 ? 2 : 0;
+    static constexpr int TY = 1 << LY, TZ = 1 << LZ;
+    // lanes on the tile's faces
+    static constexpr unsigned YL = DIM == 3 ? 0x01010101u : 0x00000001u;
+    static constexpr unsigned YH = DIM == 3 ? 0x80808080u : 0x80000000u;
+    static constexpr unsigned ZL = DIM == 3 ? 0x000000ffu : 0u;
+    static constexpr unsigned ZH = DIM == 3 ? 0xff000000u : 0u;
+};
 
 // ---------------------------------------------------------------------------
 // Local solvers (bit-exact restatements; no FMA contraction)
@@ -692,7 +729,13 @@ __global__ void __launch_bounds__(BLOCK) k_prep(KP p, bool copy_phi, bool build_
         const uint32_t src = __ballot_sync(FULL, in && st == ST_SOURCE);
         if (lane == 0) {
             const bool gh = ghost_plane(p, q.z);
-            p.Fb[w] = gh ? FULL : (blk | src | ~q.rowm);  // lanes outside the row count as fixed
+            const uint32_t fw = gh ? FULL : (blk | src | ~q.rowm);  // lanes outside the row count as fixed
+            p.Fb[w] = fw;
+            if (p.Ft) {  // tile-major copy for the remedy tile engine
+                constexpr int LY = TileGeo<DIM>::LY, LZ = TileGeo<DIM>::LZ;
+                const uint32_t t = (((q.z >> LZ) * p.nty + (q.y >> LY)) * p.W + q.wx);
+                p.Ft[t * 32u + (((q.z & ((1u << LZ) - 1u)) << LY) | (q.y & ((1u << LY) - 1u)))] = fw;
+            }
             if (build_touched) p.Bt[w] = gh ? 0u : blk;   // ghost bits record activation requests
         }
     }
@@ -1064,24 +1107,37 @@ __global__ void __launch_bounds__(BLOCK) k_build(KP p, const real_t *__restrict_
     }
 }
 
-// Remedy set from a uint8 mask (a RemedySet built elsewhere).
+// Remedy set from uint8 masks (a RemedySet built elsewhere): the work list `cells` becomes R_0;
+// members outside it (`member` & ~cells, E/ifim.py:64-72: RemedySet.member vs .cells) never get
+// relaxed and never get enqueued (E/ifim.py:211), so they go to the tile-major St bitmap the
+// remedy's dilation excludes.
 template <int DIM>
-__global__ void __launch_bounds__(BLOCK) k_remedy_load(KP p, const uint8_t *member)
+__global__ void __launch_bounds__(BLOCK) k_remedy_load(KP p, const uint8_t *cells, const uint8_t *member)
 {
     const unsigned lane = lane_id();
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t GW = (gridDim.x * blockDim.x) >> 5;
     unsigned long long cnt = 0;
+    unsigned any_stale = 0;
     for (uint32_t w = gw; w < p.nwords; w += GW) {
         const WPos q = wpos<DIM>(p, w);
         const bool in = (q.rowm >> lane) & 1u;
-        const uint32_t m = __ballot_sync(FULL, in && member[q.c0 + lane] != 0);
+        const bool wk = in && cells[q.c0 + lane] != 0;
+        const uint32_t m = __ballot_sync(FULL, wk);
+        const uint32_t sm = member ? __ballot_sync(FULL, in && !wk && member[q.c0 + lane] != 0) : 0u;
         if (lane == 0) {
             p.R0b[w] = m;
             cnt += __popc(m);
+            if (member) {
+                constexpr int LY = TileGeo<DIM>::LY, LZ = TileGeo<DIM>::LZ;
+                const uint32_t t = (((q.z >> LZ) * p.nty + (q.y >> LY)) * p.W + q.wx);
+                p.St[t * 32u + (((q.z & ((1u << LZ) - 1u)) << LY) | (q.y & ((1u << LY) - 1u)))] = sm;
+                any_stale |= sm;
+            }
         }
     }
     if (lane == 0 && cnt) atomicAdd(&p.ctl->flagged, cnt);
+    if (lane == 0 && any_stale) atomicOr(&p.ctl->stale, 1u);
 }
 
 template <int DIM>
@@ -1376,6 +1432,284 @@ template <int DIM, int SOL>
 __global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy_mr1(KP p)
 {
     remedy_body<DIM, SOL, true>(p, nullptr);
+}
+
+// ---------------------------------------------------------------------------
+// Remedy step, tile engine (single device; E/ifim.py:164-218).  One grid
+// barrier per round and no global member list.
+//
+// A tile is one bitmap word column (32 cells in x) times 32 rows: 8 (y) x 4 (z)
+// in 3D, 32 (y) in 2D; lane l of a warp owns row l.  The remedy's bitmaps are
+// tile-major, so a tile's 32 row words are one 128-byte line.  Round r:
+//   * warps take chunks of RT_CHUNK consecutive tiles from RT_SHARDS sharded
+//     counters (contiguous tile ranges, so concurrently processed tiles are
+//     spatial neighbours), and skip tiles R_r cannot touch: R_r = D_{r-1} u
+//     (N(D_{r-1}) \ fixed) meets tile t only if t's own D_{r-1} line, or a face
+//     neighbour's line with bits on the shared face, is non-empty.  Each tile's
+//     D line carries a stamp ((round + 1) << 7 | face bits), written with the
+//     line, so stale lines of earlier rounds are never read and never cleared;
+//   * the warp forms the tile's R_r rows (x-dilation in-register, y/z dilation
+//     by shuffles plus the face rows of the neighbour lines), expands the
+//     members into a warp-private shared-memory list, and relaxes them 32 at a
+//     time: gather, local solve, decrease test (E/ifim.py:203), write, D bit by
+//     a shared-memory atomicOr on the row word;
+//   * the tile's D_r line and stamp are plain stores (the tile has one owner).
+// |R_r| and |D_r| are summed per CTA and added once per round; the loop ends
+// when D_r is empty (R_{r+1} = 0).  Round 0 reads R_0 from the build's
+// row-major bitmap.
+// ---------------------------------------------------------------------------
+template <int DIM>
+__device__ __forceinline__ void tile_xyz(const KP &p, uint32_t t, uint32_t &wx, uint32_t &ty, uint32_t &tz)
+{
+    const uint32_t tyz = fdiv(t, p.fW);
+    wx = t - tyz * p.W;
+    if (DIM == 3) {
+        tz = fdiv(tyz, p.fnty);
+        ty = tyz - tz * p.nty;
+    } else {
+        tz = 0;
+        ty = tyz;
+    }
+}
+
+template <int DIM, int SOL>
+__device__ __forceinline__ void rt_tile(const KP &p, uint32_t t, uint32_t r, uint32_t vm, const real_t *__restrict__ Pc,
+                                        real_t *__restrict__ Pn, const uint32_t *__restrict__ Dp,
+                                        uint32_t *__restrict__ Dc, uint32_t *__restrict__ stc, uint16_t *buf,
+                                        uint32_t *sD, const uint32_t *__restrict__ St, unsigned &a_mem,
+                                        unsigned &a_dec)
+{
+    using G = TileGeo<DIM>;
+    const unsigned lane = lane_id();
+    uint32_t wx, ty, tz;
+    tile_xyz<DIM>(p, t, wx, ty, tz);
+    const uint32_t ny = (uint32_t)p.ny, nz = (uint32_t)p.nz, nx = p.nx32;
+    const uint32_t ly = lane & (G::TY - 1), lz = lane >> G::LY;
+    const uint32_t yb = ty << G::LY, zb = tz << G::LZ;
+    const uint32_t y = yb + ly, z = zb + lz;
+    const uint32_t WNTY = p.W * p.nty;
+    uint32_t R, carry;
+    if (r == 0) {
+        R = (y < ny && z < nz) ? __ldcg(p.R0b + (z * ny + y) * p.W + wx) : 0u;
+        carry = 0;
+    } else {
+        const uint32_t *L = Dp + t * 32u + lane;
+        const uint32_t c = (vm & 1u) ? __ldcg(L) : 0u;
+        const uint32_t dw = (vm & 2u) ? __ldcg(L - 32) : 0u;
+        const uint32_t de = (vm & 4u) ? __ldcg(L + 32) : 0u;
+        const uint32_t ys = ((vm & 8u) && ly == 0) ? __ldcg(L - p.W * 32u + (G::TY - 1)) : 0u;
+        const uint32_t yn = ((vm & 16u) && ly == G::TY - 1) ? __ldcg(L + p.W * 32u - (G::TY - 1)) : 0u;
+        uint32_t zd = 0, zu = 0;
+        if (DIM == 3) {
+            zd = ((vm & 32u) && lz == 0) ? __ldcg(L - WNTY * 32u + (G::TZ - 1) * G::TY) : 0u;
+            zu = ((vm & 64u) && lz == G::TZ - 1) ? __ldcg(L + WNTY * 32u - (G::TZ - 1) * G::TY) : 0u;
+        }
+        const uint32_t F = __ldg(p.Ft + t * 32u + lane) | (St ? __ldg(St + t * 32u + lane) : 0u);
+        uint32_t sv = __shfl_up_sync(FULL, c, 1), nv = __shfl_down_sync(FULL, c, 1);
+        if (ly == 0) sv = ys;
+        if (ly == G::TY - 1) nv = yn;
+        uint32_t dil = (c << 1) | (c >> 1) | (dw >> 31) | (de << 31) | sv | nv;
+        if (DIM == 3) {
+            uint32_t dv = __shfl_up_sync(FULL, c, G::TY), uv = __shfl_down_sync(FULL, c, G::TY);
+            if (lz == 0) dv = zd;
+            if (lz == G::TZ - 1) uv = zu;
+            dil |= dv | uv;
+        }
+        R = c | (dil & ~F);
+        carry = c;
+    }
+    // members: warp scan of the row counts, expansion into the warp's shared list
+    const uint32_t cnt = __popc(R);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(FULL, inc, o);
+        if (lane >= (unsigned)o) inc += v;
+    }
+    const uint32_t T = __shfl_sync(FULL, inc, 31);
+    if (T == 0) return;
+    const uint32_t off = inc - cnt;
+    unsigned todo = __ballot_sync(FULL, R != 0);
+    const uint32_t lt = (1u << lane) - 1u;
+    while (todo) {
+        const int src = __ffs(todo) - 1;
+        todo &= todo - 1;
+        const uint32_t bits = __shfl_sync(FULL, R, src);
+        const uint32_t cb = __shfl_sync(FULL, carry, src);
+        const uint32_t o = __shfl_sync(FULL, off, src);
+        if ((bits >> lane) & 1u)
+            buf[o + __popc(bits & lt)] = (uint16_t)((((cb >> lane) & 1u) << 10) | ((uint32_t)src << 5) | lane);
+    }
+    sD[lane] = 0;
+    __syncwarp();
+    const uint32_t x0 = wx * 32u;
+    unsigned ndec = 0;
+    for (uint32_t b = 0; b < T; b += 32) {
+        const uint32_t i = b + lane;
+        const bool live = i < T;
+        const uint32_t e = live ? (uint32_t)buf[i] : 0u;
+        const uint32_t row = (e >> 5) & 31u, bit = e & 31u;
+        const uint32_t x = x0 + bit, yy = yb + (row & (G::TY - 1)), zz = zb + (row >> G::LY);
+        const uint32_t c = DIM == 3 ? (zz * ny + yy) * nx + x : yy * nx + x;
+        Sten s;
+        s.c = s.w = s.e = s.s = s.n = s.d = s.u = INFINITY;
+        s.k = R_ONE;
+        if (live) {
+            s.c = __ldca(Pc + c);
+            if (x > 0) s.w = __ldca(Pc + (c - 1));
+            if (x + 1 < nx) s.e = __ldca(Pc + (c + 1));
+            if (yy > 0) s.s = __ldca(Pc + (c - nx));
+            if (yy + 1 < ny) s.n = __ldca(Pc + (c + nx));
+            if (DIM == 3) {
+                if (zz > 0) s.d = __ldca(Pc + (c - p.plane32));
+                if (zz + 1 < nz) s.u = __ldca(Pc + (c + p.plane32));
+            }
+            s.k = coef<SOL>(p, c);
+        }
+        bool dec = false;
+        if (live) {
+            const real_t v = solve<DIM, SOL>(p, s);
+            dec = v < s.c - tol_at(p.tol, s.c);  // E/ifim.py:203
+            if (dec) {
+                Pn[c] = v;
+                atomicOr(sD + row, 1u << bit);
+            } else if (e >> 10) {
+                Pn[c] = s.c;  // changed last round: carry into the other buffer
+            }
+        }
+        ndec += __popc(__ballot_sync(FULL, dec));
+    }
+    __syncwarp();
+    const uint32_t Dn = sD[lane];
+    const unsigned anyb = __ballot_sync(FULL, Dn != 0);
+    if (anyb) {
+        Dc[t * 32u + lane] = Dn;
+        const unsigned xl = __ballot_sync(FULL, Dn & 1u), xh = __ballot_sync(FULL, Dn >> 31);
+        if (lane == 0) {
+            const uint32_t faces = FS_SELF | (xl ? FS_XL : 0) | (xh ? FS_XH : 0) | ((anyb & G::YL) ? FS_YL : 0) |
+                                   ((anyb & G::YH) ? FS_YH : 0) | ((anyb & G::ZL) ? FS_ZL : 0) |
+                                   ((anyb & G::ZH) ? FS_ZH : 0);
+            stc[t] = ((r + 1u) << 7) | faces;
+        }
+    }
+    a_mem += T;
+    a_dec += ndec;
+}
+
+template <int DIM, int SOL>
+__global__ void __launch_bounds__(BLOCK, RT_MINB) k_remedy_t(KP p, const unsigned *skip)
+{
+    __shared__ uint16_t s_buf[WPB][1024];
+    __shared__ uint32_t s_D[WPB][32];
+    __shared__ unsigned long long sred[WPB];
+    if (skip && *skip) return;
+    Ctl *ctl = p.ctl;
+    const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
+    const bool lead = blockIdx.x == 0 && threadIdx.x == 0;
+    const uint32_t *St = vload(&ctl->stale) ? p.St : nullptr;
+    const unsigned long long r0 = vload(&ctl->flagged);
+    if (r0 == 0) return;  // empty remedy set: zero rounds
+    if (lead) {
+        ctl->peak = r0;
+        ctl->sum = 0;
+    }
+    const uint32_t K = RT_SHARDS, CH = RT_CHUNK;
+    const uint32_t shs = p.rt_shs;
+    // lane s: shard s's chunk count
+    const uint32_t sb = min(p.ntiles, lane * shs), se = min(p.ntiles, (lane + 1) * shs);
+    const uint32_t my_nch = (se - sb + CH - 1) / CH;
+    const uint32_t gw = blockIdx.x * WPB + warp;
+    const uint32_t WNTY = p.W * p.nty;
+    uint16_t *buf = s_buf[warp];
+    uint32_t *sD = s_D[warp];
+    for (uint32_t r = 0;; ++r) {
+        const int par = (int)(r & 1);
+        const real_t *__restrict__ Pc = par ? p.P1 : p.P0;
+        real_t *__restrict__ Pn = par ? p.P0 : p.P1;
+        uint32_t *Dc = par ? p.Dt1 : p.Dt0;
+        const uint32_t *Dp = par ? p.Dt0 : p.Dt1;
+        uint32_t *stc = par ? p.stamp1 : p.stamp0;
+        const uint32_t *stp = par ? p.stamp0 : p.stamp1;
+        unsigned *Gc = p.grab + (r % 3) * K * RT_GS;
+        unsigned a_mem = 0, a_dec = 0;
+        uint32_t s = gw % K;
+        while (true) {
+            uint32_t k = 0;
+            if (lane == 0) k = atomicAdd(Gc + s * RT_GS, 1u);
+            k = __shfl_sync(FULL, k, 0);
+            if (k >= __shfl_sync(FULL, my_nch, s)) {  // shard s is done: look for one with chunks left
+                const uint32_t g = vload(Gc + lane * RT_GS);
+                const unsigned left = __ballot_sync(FULL, g < my_nch);
+                if (!left) break;
+                const unsigned hi = left & (~0u << s);
+                s = __ffs(hi ? hi : left) - 1;
+                continue;
+            }
+            const uint32_t tb = s * shs + k * CH, te = min(tb + CH, min(p.ntiles, (s + 1) * shs));
+            // activity: lanes 7j + n test neighbour n of tile tb + j (stamps of round r - 1)
+            unsigned mask = 0;
+            if (r > 0) {
+                const uint32_t jj = lane / 7u, nn = lane - jj * 7u, tt = tb + jj;
+                bool f = false;
+                if (jj < CH && tt < te) {
+                    uint32_t wx, ty, tz;
+                    tile_xyz<DIM>(p, tt, wx, ty, tz);
+                    uint32_t nb = tt, need = FS_SELF;
+                    bool ex = true;
+                    switch (nn) {
+                        case 1: ex = wx > 0; nb = tt - 1; need = FS_XH; break;
+                        case 2: ex = wx + 1 < p.W; nb = tt + 1; need = FS_XL; break;
+                        case 3: ex = ty > 0; nb = tt - p.W; need = FS_YH; break;
+                        case 4: ex = ty + 1 < p.nty; nb = tt + p.W; need = FS_YL; break;
+                        case 5: ex = DIM == 3 && tz > 0; nb = tt - WNTY; need = FS_ZH; break;
+                        case 6: ex = DIM == 3 && tz + 1 < p.ntz; nb = tt + WNTY; need = FS_ZL; break;
+                        default: break;
+                    }
+                    if (ex) {
+                        const uint32_t st = __ldcg(stp + nb);
+                        f = (st >> 7) == r && (st & need);
+                    }
+                }
+                mask = __ballot_sync(FULL, f);
+            }
+            for (uint32_t t = tb, j = 0; t < te; ++t, ++j) {
+                const uint32_t vm = (mask >> (7 * j)) & 0x7fu;
+                if (r > 0 && !vm) continue;
+                rt_tile<DIM, SOL>(p, t, r, vm, Pc, Pn, Dp, Dc, stc, buf, sD, St, a_mem, a_dec);
+            }
+        }
+        const unsigned long long tm = block_sum(lane == 0 ? (unsigned long long)a_mem : 0ull, sred);
+        const unsigned long long td = block_sum(lane == 0 ? (unsigned long long)a_dec : 0ull, sred);
+        if (threadIdx.x == 0) {
+            if (tm) atomicAdd(&ctl->cnt[r % 3], tm);
+            if (td) {
+                atomicAdd(&ctl->dsum[r % 3], td);
+                atomicAdd(&ctl->writes, td);
+            }
+        }
+        if (blockIdx.x == 0) {
+            // slot (r+1)%3 of the counts was last read at the start of round r-1; grab slot (r+2)%3
+            // was last used in round r-1
+            if (threadIdx.x == 0) {
+                ctl->cnt[(r + 1) % 3] = 0;
+                ctl->dsum[(r + 1) % 3] = 0;
+            }
+            if (threadIdx.x < K) p.grab[((r + 2) % 3) * K * RT_GS + threadIdx.x * RT_GS] = 0;
+        }
+        if (!grid_barrier(ctl)) return;
+        const unsigned long long mg = vload(&ctl->cnt[r % 3]);  // |R_r|
+        const unsigned long long dg = vload(&ctl->dsum[r % 3]);  // |D_r|
+        if (lead) {
+            ctl->iters = r + 1;
+            ctl->sum += mg;
+            if (mg > ctl->peak) ctl->peak = mg;
+        }
+        if (dg == 0) break;  // R_{r+1} is empty
+        if (r + 1 >= (uint32_t)p.cap) {  // E/ifim.py:185-189
+            if (lead) ctl->err = EIK_ECAP;
+            break;
+        }
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1745,6 +2079,8 @@ struct Layout {
     size_t off_phi2, off_dd, off_bt, off_l0, off_l1, off_l2;
     size_t off_r0, off_d0, off_d1, off_f, off_lab;
     size_t off_hist, off_ctl_u, off_ctl_r, off_kps, total;
+    size_t off_ft, off_sb, off_dt0, off_dt1, off_st0, off_st1, off_grab;  // remedy tile engine
+    uint32_t tnty, tntz, ntiles;
     int64_t cap_upd, cap_rem;
 };
 
@@ -1788,6 +2124,23 @@ int make_layout(const eik_geom *g, Layout &L)
     L.off_ctl_u = o; o += al(sizeof(Ctl));
     L.off_ctl_r = o; o += al(sizeof(Ctl));
     L.off_kps = o; o += al(2 * EIK_MAX_RANKS * sizeof(KP));
+    // remedy tile engine: 32 x-cells x (8 y x 4 z) rows per tile in 3D, 32 x 32 in 2D
+    {
+        const int ly = g->ndim == 3 ? 3 : 5, lz = g->ndim == 3 ? 2 : 0;
+        L.tnty = (uint32_t)((g->ny + (1 << ly) - 1) >> ly);
+        L.tntz = (uint32_t)((g->nz + (1 << lz) - 1) >> lz);
+        const int64_t nt = W * (int64_t)L.tnty * L.tntz;
+        if (nt * 32 >= ((int64_t)1 << 32)) return fail(EIK_EINVAL, "grid too large for the tile bitmaps");
+        L.ntiles = (uint32_t)nt;
+        const size_t tb = (size_t)nt * 32 * 4;
+        L.off_ft = o; o += al(tb);
+        L.off_sb = o; o += al(tb);
+        L.off_dt0 = o; o += al(tb);
+        L.off_dt1 = o; o += al(tb);
+        L.off_st0 = o; o += al((size_t)nt * 4);
+        L.off_st1 = o; o += al((size_t)nt * 4);
+        L.off_grab = o; o += al((size_t)3 * 32 * RT_GS * 4);
+    }
     // member-list traversal (word_at): 3D groups of 4x4 rows, 2D groups of 16 rows, per x-word
     if (g->ndim == 3) {
         L.nty4 = (uint32_t)((g->ny + (1 << TILE_LY) - 1) >> TILE_LY);
@@ -1847,6 +2200,18 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, real_t *phi, const real
     p.D1b = (uint32_t *)(b + L.off_d1);
     p.Fb = (uint32_t *)(b + L.off_f);
     p.lab = (uint8_t *)(b + L.off_lab);
+    p.nty = L.tnty;
+    p.ntz = L.tntz;
+    p.ntiles = L.ntiles;
+    p.rt_shs = (L.ntiles + RT_SHARDS - 1) / RT_SHARDS;
+    p.fnty = make_fastdiv(L.tnty);
+    p.Ft = (uint32_t *)(b + L.off_ft);
+    p.St = (uint32_t *)(b + L.off_sb);
+    p.Dt0 = (uint32_t *)(b + L.off_dt0);
+    p.Dt1 = (uint32_t *)(b + L.off_dt1);
+    p.stamp0 = (uint32_t *)(b + L.off_st0);
+    p.stamp1 = (uint32_t *)(b + L.off_st1);
+    p.grab = (unsigned *)(b + L.off_grab);
     return p;
 }
 
@@ -1876,13 +2241,14 @@ template <typename K>
 int coop_launch(K kernel, KP &p, const unsigned *skip, bool with_skip, cudaStream_t st, const char *env_name,
                 int default_per_sm)
 {
-    int per_sm = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, BLOCK, 0);
+    int occ = 0;
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, BLOCK, 0);
     if (e != cudaSuccess) return fail(EIK_ECUDA, "occupancy: %s", cudaGetErrorString(e));
-    if (default_per_sm > 0 && default_per_sm < per_sm) per_sm = default_per_sm;
-    if (const char *env = getenv(env_name)) {  // tuning override
+    int per_sm = (default_per_sm > 0 && default_per_sm < occ) ? default_per_sm : occ;
+    if (const char *env = getenv(env_name)) {  // tuning override, bounded only by the occupancy limit
         const int v = atoi(env);
-        if (v > 0 && v < per_sm) per_sm = v;
+        if (v > 0 && v <= occ) per_sm = v;
+        else if (v > occ) fprintf(stderr, "[eik] %s=%d exceeds the occupancy limit %d; using %d\n", env_name, v, occ, per_sm);
     }
     if (per_sm < 1) return fail(EIK_ECUDA, "persistent kernel cannot be resident");
     dim3 grid(per_sm * num_sms()), block(BLOCK);
@@ -1918,6 +2284,7 @@ struct Engine {
     static int prep(KP &p, bool copy_phi, bool touched, cudaStream_t st)
     {
         const int grid = stream_grid(p.nwords);
+        if (p.Ft) CK(cudaMemsetAsync(p.Ft, 0xff, (size_t)p.ntiles * 32 * 4, st));  // padding rows: fixed
         if (SOL == SOL_A2) k_prep<DIM, false><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched);
         else k_prep<DIM, true><<<grid, BLOCK, 0, st>>>(p, copy_phi, touched);
         CK(cudaGetLastError());
@@ -1955,11 +2322,12 @@ struct Engine {
         CK(cudaGetLastError());
         return EIK_OK;
     }
-    static int load(KP &p, const uint8_t *member, cudaStream_t st)
+    static int load(KP &p, const uint8_t *cells, const uint8_t *member, cudaStream_t st)
     {
         int rc = reset_set(p, st);
         if (rc) return rc;
-        k_remedy_load<DIM><<<stream_grid(p.nwords), BLOCK, 0, st>>>(p, member);
+        if (member) CK(cudaMemsetAsync(p.St, 0, (size_t)p.ntiles * 32 * 4, st));  // padding rows
+        k_remedy_load<DIM><<<stream_grid(p.nwords), BLOCK, 0, st>>>(p, cells, member);
         CK(cudaGetLastError());
         return EIK_OK;
     }
@@ -1994,6 +2362,18 @@ struct Engine {
     static int remedy(KP &p, const unsigned *skip, cudaStream_t st)
     {
         return coop_launch(k_remedy<DIM, SOL>, p, skip, true, st, "EIK_REM_BLOCKS_PER_SM", 0);
+    }
+    // single device: EIK_REMEDY=list (member-list kernel) or tile (tile engine); hand-built sets
+    // with members outside their work list need the tile engine
+    static int remedy_single(KP &p, const unsigned *skip, cudaStream_t st, bool need_tile = false)
+    {
+        const char *mode = getenv("EIK_REMEDY");
+        const bool tile = need_tile || (mode ? strcmp(mode, "list") != 0 : REMEDY_TILE_DEFAULT);
+        if (!tile) return remedy(p, skip, st);
+        CK(cudaMemsetAsync(p.stamp0, 0, (size_t)p.ntiles * 4, st));
+        CK(cudaMemsetAsync(p.stamp1, 0, (size_t)p.ntiles * 4, st));
+        CK(cudaMemsetAsync(p.grab, 0, (size_t)3 * 32 * RT_GS * 4, st));
+        return coop_launch(k_remedy_t<DIM, SOL>, p, skip, true, st, "EIK_REM_BLOCKS_PER_SM", 0);
     }
 };
 
@@ -2183,25 +2563,32 @@ int EIK_FN(eik_build_remedy)(const eik_geom *g, const real_t *phi, const real_t 
     return EIK_OK;
 }
 
-int EIK_FN(eik_remedy_load)(const eik_geom *g, const uint8_t *member, const uint8_t *state, void *workspace,
-                    size_t workspace_bytes, int64_t *count, void *stream)
+int EIK_FN(eik_remedy_load_set)(const eik_geom *g, const uint8_t *cells, const uint8_t *member, const uint8_t *state,
+                                void *workspace, size_t workspace_bytes, int64_t *count, void *stream)
 {
     Layout L;
     int rc = make_layout(g, L);
     if (rc) return rc;
     if ((rc = check_ws(L, workspace, workspace_bytes))) return rc;
-    if (!member) return fail(EIK_EINVAL, "null member mask");
+    if (!cells) return fail(EIK_EINVAL, "null work-list mask");
     cudaStream_t st = (cudaStream_t)stream;
     char *b = (char *)workspace;
     Ctl *ctl = (Ctl *)(b + L.off_ctl_r);
     KP p = make_kp(g, L, workspace, nullptr, nullptr, state, 1e-12, ctl, L.cap_rem);
-    rc = dispatch(g, [&](auto E) { return E.load(p, member, st); });
+    rc = dispatch(g, [&](auto E) { return E.load(p, cells, member, st); });
     if (rc) return rc;
     Ctl c;
     CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (count) *count = (int64_t)c.flagged;
     return EIK_OK;
+}
+
+int EIK_FN(eik_remedy_load)(const eik_geom *g, const uint8_t *member, const uint8_t *state, void *workspace,
+                    size_t workspace_bytes, int64_t *count, void *stream)
+{
+    if (!member) return fail(EIK_EINVAL, "null member mask");
+    return EIK_FN(eik_remedy_load_set)(g, member, nullptr, state, workspace, workspace_bytes, count, stream);
 }
 
 int EIK_FN(eik_remedy_export)(const eik_geom *g, void *workspace, size_t workspace_bytes, uint8_t *member, void *stream)
@@ -2240,11 +2627,14 @@ int EIK_FN(eik_remedy_step)(const eik_geom *g, real_t *phi, const real_t *speed,
     Events ev;
     ev.rec(0, st);
     KP p = make_kp(g, L, workspace, phi, speed, state, tol, ctl, L.cap_rem);
+    unsigned stale = 0;  // a hand-built set with members outside its work list (eik_remedy_load_set)
+    CK(cudaMemcpyAsync(&stale, &ctl->stale, sizeof(stale), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
     // staged call: the caller may have edited phi since the last call
     rc = dispatch(g, [&](auto E) {
         int r = E.prep(p, true, false, st);
         if (r) return r;
-        return E.remedy(p, nullptr, st);
+        return E.remedy_single(p, nullptr, st, stale != 0);
     });
     if (rc) return rc;
     ev.rec(1, st);
@@ -2295,7 +2685,7 @@ int EIK_FN(eik_ifim_solve)(const eik_geom *g, real_t *phi, const real_t *speed, 
     rc = dispatch(g, [&](auto E) { return E.build(p, phi, skip, st); });
     if (rc) return rc;
     ev.rec(2, st);
-    rc = dispatch(g, [&](auto E) { return E.remedy(p, skip, st); });
+    rc = dispatch(g, [&](auto E) { return E.remedy_single(p, skip, st); });
     if (rc) return rc;
     ev.rec(3, st);
     launches += 2;

@@ -1,13 +1,13 @@
-"""Field snapshots.
+"""Binary field snapshots.
 
-``export_field_csv`` / ``import_field_csv`` keep the reference's text format
-(E/harness.py:326-380: a geometry line, then ``i,j,phi`` rows with repr
-values, bit-exact round trip) for 2D grids.  At 512^3-1024^3 a text file is
-infeasible (1e9 rows), so ``export_field_npy`` / ``import_field_npy`` write the
-same content as a raw float64 ``.npy`` array plus a JSON geometry sidecar,
-streamed plane-chunk by plane-chunk from the device (no full host copy of the
-field), and read it back memory-mapped.  Like the CSV import, the returned grid
-is a field container: unit speed, all-FAR state.
+The reference's text format (E/harness.py:326-380, CSV rows ``i,j,phi``) is out
+of scope here and infeasible at 512^3-1024^3 (1e9 rows);
+small 2D fields can still go through the reference's own exporter.
+``export_field_npy`` / ``import_field_npy`` write the field as a raw float64
+``.npy`` array plus a JSON geometry sidecar, streamed plane-chunk by
+plane-chunk from the device (no full host copy of the field), and read it back
+memory-mapped.  The returned grid is a field container: unit speed, all-FAR
+state.
 """
 from __future__ import annotations
 
@@ -19,51 +19,6 @@ import torch
 from .grid import Grid, Grid3D, new_grid
 
 _CHUNK_BYTES = 1 << 28
-
-
-def export_field_csv(grid: Grid, path: str) -> None:
-    """E/harness.py:326-342 (2D)."""
-    if getattr(grid, "ndim", 2) != 2:
-        raise ValueError("the CSV snapshot format is 2D (use export_field_npy for 3D fields)")
-    phi = grid.phi.detach().cpu().numpy() if isinstance(grid.phi, torch.Tensor) else np.asarray(grid.phi)
-    with open(path, "w", encoding="ascii") as fh:
-        fh.write(f"{grid.nx},{grid.ny},{grid.dx!r},{grid.dy!r},{grid.origin[0]!r},{grid.origin[1]!r}\n")
-        for j in range(grid.ny):
-            for i in range(grid.nx):
-                fh.write(f"{i},{j},{float(phi[j, i])!r}\n")
-
-
-def import_field_csv(path: str) -> Grid:
-    """E/harness.py:345-380: geometry + phi; unit speed, all-FAR state; malformed input raises."""
-    with open(path, "r", encoding="ascii") as fh:
-        header = fh.readline()
-        parts = header.strip().split(",")
-        if len(parts) != 6:
-            raise ValueError(f"{path}:1: expected 6 header fields nx,ny,dx,dy,x0,y0, got {len(parts)}")
-        try:
-            nx, ny = int(parts[0]), int(parts[1])
-            dx, dy, x0, y0 = (float(p) for p in parts[2:])
-        except ValueError:
-            raise ValueError(f"{path}:1: malformed header {header.strip()!r}") from None
-        grid = new_grid(nx, ny, dx, dy, origin=(x0, y0), speed=1.0)
-        count = 0
-        for lineno, line in enumerate(fh, start=2):
-            if not line.strip():
-                continue
-            fields = line.strip().split(",")
-            if len(fields) != 3:
-                raise ValueError(f"{path}:{lineno}: expected i,j,phi, got {line.strip()!r}")
-            try:
-                i, j, value = int(fields[0]), int(fields[1]), float(fields[2])
-            except ValueError:
-                raise ValueError(f"{path}:{lineno}: malformed row {line.strip()!r}") from None
-            if not (0 <= i < nx and 0 <= j < ny):
-                raise ValueError(f"{path}:{lineno}: cell ({i}, {j}) outside {nx}x{ny} grid")
-            grid.phi[j, i] = value
-            count += 1
-        if count != nx * ny:
-            raise ValueError(f"{path}: expected {nx * ny} cell rows, found {count}")
-    return grid
 
 
 def _geometry(grid) -> dict:

@@ -134,12 +134,11 @@ class _HostResult:
     Large fields: the copy is allocated on a helper thread while the device
     solves (the engine call releases the GIL).  A pinned caller array gets a
     pinned copy (torch's caching host allocator reuses freed ones) filled by a
-    second device-to-host DMA, so no host memcpy is on the critical path; a
-    pageable caller array gets a first-touched pageable copy filled chunk by
-    chunk behind the device-to-host copy.
+    second device-to-host DMA, so no host memcpy is on the critical path.  A
+    pageable caller array gets a first-touched pageable copy; the field is
+    downloaded once into the caller's array and the copy is a host memcpy of it.
     """
 
-    CHUNKS = 8
     MIN_CELLS = 1 << 22
 
     def __init__(self, dg):
@@ -170,22 +169,10 @@ class _HostResult:
         buf = self.buf
         host = torch.from_numpy(gphi) if isinstance(gphi, np.ndarray) else gphi
         dev = dg.phi.reshape(host.shape)
-        stream = torch.cuda.current_stream(dg.device)
         if self.pinned:
             host.copy_(dev, non_blocking=True)
             buf.copy_(dev, non_blocking=True)
-            stream.synchronize()
-        elif host.dim() >= 1 and host.shape[0] >= self.CHUNKS and host.is_pinned():
-            bounds = np.linspace(0, host.shape[0], self.CHUNKS + 1).astype(int)
-            events = []
-            for a, b in zip(bounds[:-1], bounds[1:]):
-                host[a:b].copy_(dev[a:b], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(stream)
-                events.append(ev)
-            for (a, b), ev in zip(zip(bounds[:-1], bounds[1:]), events):
-                ev.synchronize()
-                buf[a:b].copy_(host[a:b])  # overlaps the DMA of the next chunks
+            torch.cuda.current_stream(dg.device).synchronize()
         else:
             dg.commit(phi=True)
             buf.copy_(host)
@@ -217,26 +204,61 @@ class Workspace:
         return C.c_void_p(self.buf.data_ptr())
 
 
-_WS: dict = {}
-_WS_LOCK = __import__("threading").Lock()
+_WS: "dict" = {}  # (thread id, device, geometry) -> Workspace, least recently used first
+_WS_LOCK = __import__("threading").RLock()
+_TLS = __import__("threading").local()
+
+
+class _ThreadReaper:
+    """Lives in a thread's local storage: when the thread ends, its workspaces are released."""
+
+    def __init__(self, ident):
+        self.ident = ident
+
+    def __del__(self):
+        try:
+            with _WS_LOCK:
+                for k in [k for k in _WS if k[0] == self.ident]:
+                    del _WS[k]
+        except Exception:  # noqa: BLE001  (interpreter shutdown)
+            pass
+
+
+def _ws_budget(device) -> int:
+    """Bytes all cached workspaces of one device may hold (EIKONAL_WS_BUDGET, default half the
+    device memory)."""
+    env = os.environ.get("EIKONAL_WS_BUDGET", "").strip()
+    if env:
+        return int(float(env))
+    return torch.cuda.get_device_properties(device).total_memory // 2
 
 
 def workspace(geom: _native.Geom, device: torch.device) -> Workspace:
     """The calling thread's workspace for this geometry (kept between calls: the staged API
     leaves the remedy set in it).  Per thread, so concurrent solves on different grids of the
-    same shape never share scratch memory (the reference's solvers are re-entrant)."""
+    same shape never share scratch memory (the reference's solvers are re-entrant).  A thread's
+    workspaces are released when the thread ends, and the cache of a device is bounded by a byte
+    budget (least recently used entries go first).  Evicting an entry only drops the cache's
+    reference: a call (or a RemedySet) still holding the workspace keeps its memory alive."""
     import threading
 
-    key = (threading.get_ident(), str(device), geom.nx, geom.ny, geom.nz, geom.ndim, geom.dtype)
+    ident = threading.get_ident()
+    if getattr(_TLS, "reaper", None) is None:
+        _TLS.reaper = _ThreadReaper(ident)
+    key = (ident, str(device), geom.nx, geom.ny, geom.nz, geom.ndim, geom.dtype)
     with _WS_LOCK:
-        ws = _WS.get(key)
+        ws = _WS.pop(key, None)
         if ws is None:
-            mine = [k for k in _WS if k[0] == key[0]]
-            if len(mine) >= 4:
-                for k in mine:
-                    del _WS[k]
+            n = C.c_size_t(0)
+            _native.check(_native.lib(geom.dtype).eik_workspace_size(C.byref(geom), C.byref(n)), geom.dtype)
+            budget, need = _ws_budget(device), int(n.value)
+            used = sum(w.nbytes for k, w in _WS.items() if k[1] == key[1])
+            for k in [k for k in _WS if k[1] == key[1]]:  # least recently used first, before allocating
+                if used + need <= budget:
+                    break
+                used -= _WS.pop(k).nbytes
             ws = Workspace(geom, device)
-            _WS[key] = ws
+        _WS[key] = ws  # most recently used last
     return ws
 
 
@@ -258,25 +280,33 @@ def _history_cap(g: _native.Geom) -> int:
 # ---------------------------------------------------------------------------
 
 class RemedySet:
-    """Cells flagged for repair (E/ifim.py:64-72): ``member`` mask + ``cells`` list.
+    """Cells flagged for repair (E/ifim.py:64-72): ``member`` mask + ``cells`` work list.
 
     Sets produced by build_remedy_set live on the device; ``member`` and
-    ``cells`` are materialised on first access.  A RemedySet built by hand from
-    a member mask (and/or a cell list) is accepted by ifim_remedy_step too.
+    ``cells`` are materialised on first access (``cells`` = the members in
+    ascending order, as E/ifim.py:158-161 builds it).  A RemedySet built by
+    hand follows the reference's dataclass: ``cells`` defaults to an empty
+    list, and the remedy step relaxes ``cells`` (E/ifim.py:184-193) while
+    ``member`` only decides which neighbours get enqueued (E/ifim.py:211), so
+    ``RemedySet(member=m)`` alone is an empty set and members outside ``cells``
+    are never relaxed or enqueued.  The device engine works on sets, so
+    ``cells`` must not repeat a cell and must be marked in ``member``
+    (ValueError otherwise; the reference would process such a list with
+    duplicates).
     """
 
     def __init__(self, member=None, cells=None, *, _device=None):
         self._member = member
-        self._cells = [int(c) for c in cells] if cells is not None else None
         self._dev = _device  # dict(mask, count, ws, gen, host, shape)
+        if cells is not None:
+            self._cells = [int(c) for c in cells]
+        else:
+            self._cells = None if _device is not None else []
 
     def __len__(self) -> int:
         if self._dev is not None:
             return int(self._dev["count"])
-        if self._cells is not None:
-            return len(self._cells)
-        m = self._member
-        return int(m.sum()) if m is not None else 0
+        return len(self._cells)
 
     @property
     def member(self):
@@ -287,6 +317,7 @@ class RemedySet:
 
     @member.setter
     def member(self, value):
+        self.cells  # keep the work list of a device-backed set
         self._member = value
         self._dev = None
 
@@ -294,9 +325,7 @@ class RemedySet:
     def cells(self) -> list:
         if self._cells is None:
             m = self.member
-            if m is None:
-                self._cells = []
-            elif isinstance(m, torch.Tensor):
+            if isinstance(m, torch.Tensor):
                 self._cells = torch.nonzero(m.reshape(-1)).reshape(-1).cpu().tolist()
             else:
                 self._cells = np.flatnonzero(np.asarray(m).reshape(-1)).tolist()
@@ -304,34 +333,49 @@ class RemedySet:
 
     @cells.setter
     def cells(self, value):
+        self.member  # keep the membership mask of a device-backed set
         self._cells = [int(c) for c in value]
-        self._member = None
         self._dev = None
 
     def _drain(self):
-        """After ifim_remedy_step the set is empty (E/ifim.py:186, :208)."""
+        """After ifim_remedy_step the work list is empty and its members are cleared
+        (E/ifim.py:186, :208); members outside the work list keep their mark."""
         if self._dev is not None:
             self._dev["count"] = 0
             self._dev["mask"].zero_()
-        if self._member is not None:
+        elif self._member is not None and self._cells:
+            idx = self._cells
             if isinstance(self._member, torch.Tensor):
-                self._member.zero_()
+                flat = self._member.reshape(-1)
+                flat[torch.as_tensor(idx, dtype=torch.int64, device=flat.device)] = False
             else:
-                self._member[...] = False
+                np.asarray(self._member).reshape(-1)[idx] = False
         self._cells = []
 
-    def _device_mask(self, shape, device) -> torch.Tensor:
+    def _device_masks(self, shape, device):
+        """(work-list mask, member mask or None) as flat uint8 CUDA tensors."""
         if self._dev is not None:
-            return self._dev["mask"]
+            return self._dev["mask"], None
         n = int(np.prod(shape))
-        if self._member is not None:
-            m = self._member
-            t = m if isinstance(m, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(m))
-            return t.reshape(-1).to(device=device, dtype=torch.uint8).contiguous()
-        mask = torch.zeros(n, dtype=torch.uint8, device=device)
-        if self._cells:
-            mask[torch.as_tensor(self._cells, dtype=torch.int64, device=device)] = 1
-        return mask
+        cells = self._cells
+        work = torch.zeros(n, dtype=torch.uint8, device=device)
+        if cells:
+            idx = torch.as_tensor(cells, dtype=torch.int64, device=device)
+            if int(idx.min()) < 0 or int(idx.max()) >= n:
+                raise ValueError(f"RemedySet.cells holds a cell outside the {n}-cell grid")
+            work[idx] = 1
+            if int(work.sum()) != len(cells):
+                raise ValueError("RemedySet.cells repeats a cell (the device engine relaxes sets)")
+        if self._member is None:
+            return work, None
+        m = self._member
+        t = m if isinstance(m, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(m))
+        mem = t.reshape(-1).to(device=device, dtype=torch.uint8).contiguous()
+        if mem.numel() != n:
+            raise ValueError(f"RemedySet.member has {mem.numel()} cells, the grid {n}")
+        if cells and bool(((work != 0) & (mem == 0)).any()):
+            raise ValueError("RemedySet.cells holds cells that RemedySet.member does not mark")
+        return work, mem
 
 
 # ---------------------------------------------------------------------------
@@ -404,10 +448,11 @@ def ifim_remedy_step(grid, remedy: RemedySet, tol: float = 1e-12, workers: int =
     ws = workspace(geom, dg.device)
     fresh = (remedy._dev is not None and remedy._dev.get("ws") is ws and remedy._dev.get("gen") == ws.gen)
     if not fresh:
-        mask = remedy._device_mask(tuple(grid.phi.shape), dg.device)
+        work, member = remedy._device_masks(tuple(grid.phi.shape), dg.device)
         cnt = C.c_int64(0)
-        _native.check(_native.lib(geom.dtype).eik_remedy_load(C.byref(geom), _ptr(mask), _ptr(dg.state), ws.ptr, ws.nbytes,
-                                                    C.byref(cnt), dg.stream))
+        _native.check(_native.lib(geom.dtype).eik_remedy_load_set(C.byref(geom), _ptr(work), _ptr(member),
+                                                                  _ptr(dg.state), ws.ptr, ws.nbytes, C.byref(cnt),
+                                                                  dg.stream))
     ws.gen += 1
     st = _native.Stats()
     rc = _native.lib(geom.dtype).eik_remedy_step(C.byref(geom), _ptr(dg.phi), _ptr(dg.speed), _ptr(dg.state), float(tol),

@@ -118,13 +118,26 @@ def test_no_cpu_fallback():
 
 
 def test_remedy_set_host_side():
+    """E/ifim.py:64-72: the work list is ``cells`` (default []), ``member`` only marks membership."""
     member = np.zeros(16, dtype=bool)
     member[[3, 7]] = True
     rs = eik.RemedySet(member=member)
-    assert len(rs) == 2 and rs.cells == [3, 7]
+    assert len(rs) == 0 and rs.cells == []
     rs2 = eik.RemedySet(member=member.copy(), cells=[3, 7])
+    assert len(rs2) == 2
     rs2._drain()
     assert len(rs2) == 0 and not rs2.member.any()
+    rs3 = eik.RemedySet(member=member.copy(), cells=[7])
+    rs3._drain()
+    assert rs3.member.tolist() == [i == 3 for i in range(16)]  # members outside the work list stay
+
+
+def test_remedy_set_rejects_lists_the_set_engine_cannot_mirror():
+    member = np.zeros(16, dtype=bool)
+    member[[3, 7]] = True
+    for cells in ([3, 3], [3, 5], [99]):
+        with pytest.raises(ValueError):
+            eik.RemedySet(member=member, cells=cells)._device_masks((16,), torch.device("cpu"))
 
 
 def test_resolve_devices(monkeypatch):
@@ -144,25 +157,6 @@ def test_resolve_devices(monkeypatch):
     assert resolve_devices(None) == [0, 1]
     monkeypatch.setenv("EIKONAL_DEVICES", "0,0,2")
     assert resolve_devices(None) == [0, 0, 2]
-
-
-def test_field_csv_round_trip_is_bit_exact(tmp_path):
-    """T/test_harness.py:111-121 against E/harness.py:326-380's format."""
-    g = eik.new_grid(5, 3, 0.1, 0.7, origin=(0.3, -1.0))
-    rng = np.random.default_rng(1)
-    g.phi[:] = rng.random((3, 5))
-    g.phi[1, 2] = np.inf
-    p = str(tmp_path / "f.csv")
-    eik.export_field_csv(g, p)
-    h = eik.import_field_csv(p)
-    assert (h.nx, h.ny, h.dx, h.dy, h.origin) == (5, 3, 0.1, 0.7, (0.3, -1.0))
-    assert np.array_equal(h.phi.view(np.uint64), g.phi.view(np.uint64))
-    with open(p) as fh:
-        lines = fh.read().splitlines()
-    with open(p, "w") as fh:
-        fh.write("\n".join(lines[:-1]) + "\n")
-    with pytest.raises(ValueError):
-        eik.import_field_csv(p)
 
 
 def test_field_npy_round_trip_3d(tmp_path):

@@ -125,6 +125,31 @@ def test_user_built_remedy_set(staged2d):
     assert len(rs) == 0 and not member.any()
 
 
+@pytest.mark.gpu
+def test_hand_built_remedy_sets_match_the_reference():
+    """RemedySet(member) alone is empty; members outside ``cells`` are never relaxed or enqueued
+    (E/ifim.py:64-72, :184-213); fixtures from the live reference (tests/golden/make_remedy_sets.py)."""
+    Z = np.load(os.path.join(GOLDEN, "remedy_sets.npz"))
+
+    def grid():
+        return eik.Grid(24, 24, 1.0, 1.0, (0.0, 0.0), Z["phi_in"].copy(), Z["speed"].copy(), Z["state"].copy())
+
+    g = grid()
+    st = eik.ifim_remedy_step(g, eik.RemedySet(member=Z["member"].copy()))
+    assert [st.iterations, st.solver_calls, st.peak_remedy] == Z["a_stats"].tolist()
+    assert np.array_equal(g.phi.view(np.uint64), Z["a_phi"].view(np.uint64))
+    g = grid()
+    rs = eik.RemedySet(member=Z["member"].copy(), cells=Z["b_cells"].tolist())
+    st = eik.ifim_remedy_step(g, rs)
+    assert [st.iterations, st.solver_calls, st.peak_remedy] == Z["b_stats"].tolist()
+    assert np.array_equal(g.phi.view(np.uint64), Z["b_phi"].view(np.uint64))
+    assert np.array_equal(np.asarray(rs.member), Z["b_member_after"])
+    g = grid()
+    st = eik.ifim_remedy_step(g, eik.RemedySet(member=Z["member"].copy(), cells=np.flatnonzero(Z["member"]).tolist()))
+    assert [st.iterations, st.solver_calls, st.peak_remedy] == Z["c_stats"].tolist()
+    assert np.array_equal(g.phi.view(np.uint64), Z["c_phi"].view(np.uint64))
+
+
 def test_local_solver_bitwise(local_vectors):
     L = local_vectors
     lib = _native.lib()
