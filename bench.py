@@ -275,20 +275,75 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_sample(n: int, threads: int, config: str = "cfg4"):
-    """Oracle port (C, OpenMP) on the same workload family at n^3; returns (calls, seconds)."""
-    import torch
+# bounded CPU samples (~10-20 s of work on 8-16 host cores): the oracle port's edge per config, and
+# the Python reference's (2D only, one core: the GIL) for the reference arm
+CPU_SIZE = {"cfg1": 256, "cfg2": 2048, "cfg3": 256, "cfg4": 144, "cfg5": 128}
+PYREF_SIZE = {"cfg1": 256, "cfg2": 512}
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
 
+
+def sample_label(config, n):
+    return f"{n}^2" if config in ("cfg1", "cfg2") else f"{n}^3"
+
+
+def cpu_sample(n: int, threads: int, config: str = "cfg4"):
+    """Oracle port (C, OpenMP) on the same workload at edge n; returns (calls, seconds, threads)."""
     from oracle import cpu
 
     cpu.build()
-    w = make_workload(torch, torch.device("cpu"), config, n)
-    F = w.F.numpy()
-    sd = w.linear_seeds()
+    h, F, seeds = workload_np(config, n)
+    F = np.ascontiguousarray(F)
+    sd = Workload(config, n, h, _NpShape(F), seeds, "").linear_seeds()
+    if F.size < (1 << 20):
+        threads = 1  # small grids: per-iteration thread fan-out costs more than it saves
     t0 = time.perf_counter()
-    res = cpu.solve_ifim(w.shape, w.spacing(), F, [c for c, _ in sd], [v for _, v in sd], threads=threads)
+    res = cpu.solve_ifim(F.shape, (h, h) if F.ndim == 2 else h, F, [c for c, _ in sd], [v for _, v in sd],
+                         threads=threads)
     dt = time.perf_counter() - t0
-    return res.stats["solver_calls"], dt
+    return res.stats["solver_calls"], dt, threads
+
+
+class _NpShape:
+    """Just enough of a tensor for Workload's bookkeeping."""
+
+    def __init__(self, a):
+        self.shape = a.shape
+
+    def dim(self):
+        return len(self.shape)
+
+
+def pyref_sample(n: int, config: str):
+    """The reference's own solve_ifim (the unmodified package installed in baseline/_ref, its public
+    API, workers=1) on a 2D config at edge n; returns (calls, seconds) or None if unavailable."""
+    if config not in PYREF_SIZE or not os.path.isdir(os.path.join(REF_DIR, "eikonal")):
+        return None
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    from eikonal.grid import BoundaryCondition, CellIndex, new_grid
+    from eikonal.ifim import solve_ifim
+
+    h, F, seeds = workload_np(config, n)
+    g = new_grid(n, n, h, h, origin=(0.0, 0.0), speed=np.ascontiguousarray(F))
+    bc = BoundaryCondition(tuple((CellIndex(i, j), 0.0) for i, j in seeds))
+    t0 = time.perf_counter()
+    res = solve_ifim(g, bc, workers=1)
+    return res.stats.solver_calls, time.perf_counter() - t0
+
+
+def full_size_oracle(config, n):
+    """The oracle port's full-size solve time recorded with the digests (tests/golden/fullsize.json)."""
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "fullsize.json")) as fh:
+            rec = json.load(fh).get(f"{config}@{n}")
+    except OSError:
+        return None
+    if not rec:
+        return None
+    o = rec["oracle"]
+    return {"size": sample_label(config, n), "seconds": round(o["seconds"]["total"], 2),
+            "value": o["calls_per_s"], "unit": UNIT, "threads": o["threads"], "kind": "port",
+            "where": f"authoring container ({o['cpu_count']} cores), tests/golden/make_fullsize.py"}
 
 
 def dist_setup():
@@ -299,28 +354,45 @@ def dist_setup():
 
 
 def run_reference(args):
+    """The reference arm: the reference's own implementation timed on this host.  2D configs run
+    the unmodified Python package from baseline/_ref (kind "reference", one core: the GIL);
+    3D configs (the reference has no 3D engine) run the oracle port of its
+    algorithm (kind "port", OpenMP on every host core).  Each step is one full solve of a bounded
+    sample of the configured workload."""
     world, rank, _ = dist_setup()
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
-    n = args.cpu_size
+    py = args.config in PYREF_SIZE and os.path.isdir(os.path.join(REF_DIR, "eikonal"))
+    n = args.cpu_size or (PYREF_SIZE[args.config] if py else CPU_SIZE[args.config])
+
+    def one():
+        if py:
+            c, s = pyref_sample(n, args.config)
+            return c, s, 1
+        return cpu_sample(n, threads, args.config)
+
     for _ in range(args.warmup):
-        cpu_sample(n, threads, args.config)
-    calls, secs = 0, 0.0
+        one()
+    calls, secs, used = 0, 0.0, 1
     for _ in range(args.steps):
-        c, s = cpu_sample(n, threads, args.config)
+        c, s, used = one()
         calls += c
         secs += s
     v = calls / secs
+    impl = ("reference eikonal.solve_ifim (baseline/_ref, unmodified, workers=1)" if py
+            else f"oracle/eik_oracle.c (port of E/ifim.py), OpenMP x{used}")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_desc(args.config, args.size), "size": args.size,
-                   "parallelism": "host threads", "sample_size": n},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": f"full solve_ifim of {workload_desc(args.config, n)} (same family, bounded "
-                                   f"sample of the {args.size}^3 workload), oracle/eik_oracle.c OpenMP x{threads}"},
+                   "parallelism": "host threads", "sample_size": n, "implementation": impl},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": used, "kind": "reference" if py else "port",
+                         "sample": f"full solve_ifim of {workload_desc(args.config, n)} (a bounded "
+                                   f"{sample_label(args.config, n)} sample of the {sample_label(args.config, args.size)} "
+                                   f"workload) with {impl}",
+                         "full_size": full_size_oracle(args.config, args.size)},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -699,8 +771,9 @@ def run_ours(args):
         else:
             e2e = {"value": None, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                    "note": "e2e is measured by the single-GPU run through solve_ifim"}
-        cpu_calls, cpu_s = cpu_sample(args.cpu_size, os.cpu_count() or 1, args.config) if not args.no_cpu \
-            else (0, 0.0)
+        cpu_n = args.cpu_size or CPU_SIZE[args.config]
+        cpu_calls, cpu_s, cpu_threads = cpu_sample(cpu_n, os.cpu_count() or 1, args.config) if not args.no_cpu \
+            else (0, 0.0, 0)
         out = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -725,9 +798,11 @@ def run_ours(args):
                                 for k, b in r.phase_bytes.items() if r.phase_ms.get(k)}
                                if getattr(r, "phase_bytes", None) else None),
             "cpu_baseline": {"value": (cpu_calls / cpu_s) if cpu_s else None, "unit": UNIT,
-                             "cores": os.cpu_count() or 1, "kind": "port",
-                             "sample": f"full solve of {workload_desc(args.config, args.cpu_size)} (same family) with "
-                                       f"oracle/eik_oracle.c, OpenMP x{os.cpu_count() or 1}, {cpu_s:.1f} s"},
+                             "cores": cpu_threads, "kind": "port",
+                             "sample": f"full solve of {workload_desc(args.config, cpu_n)} (a bounded "
+                                       f"{sample_label(args.config, cpu_n)} sample of the workload) with "
+                                       f"oracle/eik_oracle.c, OpenMP x{cpu_threads}, {cpu_s:.1f} s",
+                             "full_size": full_size_oracle(args.config, n)},
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
@@ -783,7 +858,8 @@ def main():
     ap.add_argument("--size", type=int, default=None, help="grid edge (default 512; cfg5: 1024)")
     ap.add_argument("--config", default="cfg4", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
                     help="BASELINE.json config (cfg4 = the headline 512^3 checkerboard)")
-    ap.add_argument("--cpu-size", type=int, default=144, help="edge of the bounded CPU sample (~10-15 s of oracle work)")
+    ap.add_argument("--cpu-size", type=int, default=None,
+                    help="edge of the bounded CPU sample (default per config: ~10-20 s of CPU work)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

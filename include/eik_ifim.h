@@ -99,6 +99,14 @@ int eik_remedy_load(const eik_geom *g, const uint8_t *member, const uint8_t *sta
 int eik_remedy_load_set(const eik_geom *g, const uint8_t *cells, const uint8_t *member, const uint8_t *state,
                         void *workspace, size_t workspace_bytes, int64_t *count, void *stream);
 
+/* Verification reductions on device fields (E/harness.py:165-179).  eik_field_max_diff: max |a - b|
+ * over n values, equal same-sign infinities count 0, NaN propagates, 0.0 for n == 0; `scratch` is
+ * 16 bytes of device memory.  eik_chunk_sha256: SHA-256 (FIPS 180-4) of every `chunk`-byte piece of
+ * the device byte range (the last one may be short) into digests[32 * pieces] (device); the
+ * package's field_digest hashes the concatenated piece digests on the host. */
+int eik_field_max_diff(const double *a, const double *b, int64_t n, void *scratch, double *out, void *stream);
+int eik_chunk_sha256(const void *data, int64_t nbytes, int64_t chunk, uint8_t *digests, void *stream);
+
 /* Write the workspace remedy set as a device uint8 mask[N]. */
 int eik_remedy_export(const eik_geom *g, void *workspace, size_t workspace_bytes, uint8_t *member,
                       void *stream);
@@ -213,6 +221,8 @@ int eik_build_remedy_f32(const eik_geom *g, const float *phi, const float *speed
                          void *workspace, size_t workspace_bytes, eik_stats *out, void *stream);
 int eik_remedy_load_f32(const eik_geom *g, const uint8_t *member, const uint8_t *state, void *workspace,
                         size_t workspace_bytes, int64_t *count, void *stream);
+int eik_field_max_diff_f32(const float *a, const float *b, int64_t n, void *scratch, double *out, void *stream);
+int eik_chunk_sha256_f32(const void *data, int64_t nbytes, int64_t chunk, uint8_t *digests, void *stream);
 int eik_remedy_load_set_f32(const eik_geom *g, const uint8_t *cells, const uint8_t *member, const uint8_t *state,
                             void *workspace, size_t workspace_bytes, int64_t *count, void *stream);
 int eik_remedy_export_f32(const eik_geom *g, void *workspace, size_t workspace_bytes, uint8_t *member, void *stream);

@@ -23,7 +23,7 @@ from .grid import (
 from .fieldio import export_field_npy, import_field_npy
 from .fim import solve_fim
 from .fixpoint import max_residual, solve_fixpoint
-from .harness import METHOD_NAMES, PARALLEL_METHODS, field_max_diff, field_sha256, run_method
+from .harness import METHOD_NAMES, PARALLEL_METHODS, field_digest, field_max_diff, field_sha256, run_method
 from .ifim import (
     RemedySet,
     build_remedy_set,
@@ -40,7 +40,7 @@ __version__ = "0.1.0"
 __all__ = [
     "INF", "BoundaryCondition", "CellIndex", "CellIndex3D", "CellState", "Grid", "Grid3D", "METHOD_NAMES",
     "PARALLEL_METHODS", "RemedySet", "RunStats", "SolverResult", "build_remedy_set", "clear_workspaces",
-    "export_field_npy", "field_max_diff", "field_sha256", "import_field_npy", "ifim_remedy_step", "ifim_update_step", "new_grid", "new_grid_3d",
+    "export_field_npy", "field_digest", "field_max_diff", "field_sha256", "import_field_npy", "ifim_remedy_step", "ifim_update_step", "new_grid", "new_grid_3d",
     "reset_field", "resolve_workers", "run_method", "seed_linear", "seed_point", "solve_fim", "solve_ifim", "solve_fixpoint",
     "max_residual",
 ]

@@ -31,6 +31,7 @@ NVCC_FLAGS = [
 
 EXPORTS = (
     "eik_workspace_size", "eik_ifim_update_step", "eik_build_remedy", "eik_remedy_load", "eik_remedy_load_set",
+    "eik_field_max_diff", "eik_chunk_sha256",
     "eik_remedy_export", "eik_remedy_step", "eik_ifim_solve", "eik_local_solve",
     "eik_last_error", "eik_version", "eik_workspace_offsets", "eik_slab_update_init", "eik_slab_update_iter",
     "eik_slab_apply_requests", "eik_slab_build", "eik_slab_remedy_round", "eik_solve_fixpoint",
@@ -90,7 +91,7 @@ class Stats(C.Structure):
 
 EXPORTS_F32 = (
     "eik_workspace_size_f32", "eik_ifim_update_step_f32", "eik_build_remedy_f32", "eik_remedy_load_f32",
-    "eik_remedy_load_set_f32",
+    "eik_remedy_load_set_f32", "eik_field_max_diff_f32", "eik_chunk_sha256_f32",
     "eik_remedy_export_f32", "eik_remedy_step_f32", "eik_ifim_solve_f32", "eik_solve_fixpoint_f32",
     "eik_max_residual_f32", "eik_local_solve_f32", "eik_last_error_f32", "eik_version_f32", "eik_solve_fim_f32",
 )
@@ -98,6 +99,15 @@ EXPORTS_F32 = (
 _lib = None
 _lib32 = None
 _last_dtype = EIK_F64
+
+
+def _bind(L, name, argtypes):
+    """Set a symbol's argtypes; a symbol missing from an older build stays unbound (calling it
+    raises AttributeError) instead of breaking the whole library load."""
+    try:
+        getattr(L, name).argtypes = argtypes
+    except AttributeError:
+        pass
 
 
 class _Suffixed:
@@ -125,28 +135,30 @@ def lib(dtype: int = EIK_F64):
     L = C.CDLL(LIB)
     P, i64, dbl, vp = C.c_void_p, C.c_int64, C.c_double, C.c_void_p
     GP, SP = C.POINTER(Geom), C.POINTER(Stats)
-    L.eik_workspace_size.argtypes = [GP, C.POINTER(C.c_size_t)]
-    L.eik_ifim_update_step.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]
-    L.eik_build_remedy.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, SP, vp]
-    L.eik_remedy_load.argtypes = [GP, P, P, P, C.c_size_t, C.POINTER(i64), vp]
-    L.eik_remedy_load_set.argtypes = [GP, P, P, P, P, C.c_size_t, C.POINTER(i64), vp]
-    L.eik_remedy_export.argtypes = [GP, P, C.c_size_t, P, vp]
-    L.eik_remedy_step.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, SP, vp]
-    L.eik_ifim_solve.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]
-    L.eik_local_solve.argtypes = [C.c_int, P, P, P, P, dbl, dbl, P, i64, vp]
-    L.eik_workspace_offsets.argtypes = [GP, P]
-    L.eik_slab_update_init.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, C.POINTER(i64), vp]
-    L.eik_slab_update_iter.argtypes = [GP, P, P, P, dbl, i64, P, C.c_size_t, vp]
-    L.eik_slab_apply_requests.argtypes = [GP, P, P, i64, P, C.c_size_t, C.POINTER(i64), vp]
-    L.eik_slab_build.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, C.POINTER(i64), C.POINTER(i64), vp]
-    L.eik_slab_remedy_round.argtypes = [GP, P, P, P, dbl, i64, P, C.c_size_t, C.POINTER(i64), C.POINTER(i64), vp]
-    L.eik_solve_fixpoint.argtypes = [GP, P, P, P, P, P, i64, dbl, i64, P, C.c_size_t, SP, vp]
-    L.eik_max_residual.argtypes = [GP, P, P, P, P, C.c_size_t, C.POINTER(dbl), vp]
-    L.eik_solve_fim.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, SP, vp]
+    _bind(L, "eik_workspace_size", [GP, C.POINTER(C.c_size_t)])
+    _bind(L, "eik_ifim_update_step", [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp])
+    _bind(L, "eik_build_remedy", [GP, P, P, P, dbl, P, C.c_size_t, SP, vp])
+    _bind(L, "eik_remedy_load", [GP, P, P, P, C.c_size_t, C.POINTER(i64), vp])
+    _bind(L, "eik_remedy_load_set", [GP, P, P, P, P, C.c_size_t, C.POINTER(i64), vp])
+    _bind(L, "eik_field_max_diff", [P, P, i64, P, C.POINTER(dbl), vp])
+    _bind(L, "eik_chunk_sha256", [P, i64, i64, P, vp])
+    _bind(L, "eik_remedy_export", [GP, P, C.c_size_t, P, vp])
+    _bind(L, "eik_remedy_step", [GP, P, P, P, dbl, P, C.c_size_t, SP, vp])
+    _bind(L, "eik_ifim_solve", [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp])
+    _bind(L, "eik_local_solve", [C.c_int, P, P, P, P, dbl, dbl, P, i64, vp])
+    _bind(L, "eik_workspace_offsets", [GP, P])
+    _bind(L, "eik_slab_update_init", [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, C.POINTER(i64), vp])
+    _bind(L, "eik_slab_update_iter", [GP, P, P, P, dbl, i64, P, C.c_size_t, vp])
+    _bind(L, "eik_slab_apply_requests", [GP, P, P, i64, P, C.c_size_t, C.POINTER(i64), vp])
+    _bind(L, "eik_slab_build", [GP, P, P, P, dbl, P, C.c_size_t, C.POINTER(i64), C.POINTER(i64), vp])
+    _bind(L, "eik_slab_remedy_round", [GP, P, P, P, dbl, i64, P, C.c_size_t, C.POINTER(i64), C.POINTER(i64), vp])
+    _bind(L, "eik_solve_fixpoint", [GP, P, P, P, P, P, i64, dbl, i64, P, C.c_size_t, SP, vp])
+    _bind(L, "eik_max_residual", [GP, P, P, P, P, C.c_size_t, C.POINTER(dbl), vp])
+    _bind(L, "eik_solve_fim", [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, SP, vp])
     RP = C.POINTER(Rank)
-    L.eik_mr_prepare.argtypes = [GP, C.c_int32, RP, C.c_int32, C.c_int32, P, P, P, P, i64, dbl, vp]
-    L.eik_mr_run.argtypes = [GP, C.c_int32, RP, C.c_int32, C.c_int32, P, P, dbl, P, i64, SP, vp]
-    L.eik_peer_enable.argtypes = [C.c_int32, C.c_int32]
+    _bind(L, "eik_mr_prepare", [GP, C.c_int32, RP, C.c_int32, C.c_int32, P, P, P, P, i64, dbl, vp])
+    _bind(L, "eik_mr_run", [GP, C.c_int32, RP, C.c_int32, C.c_int32, P, P, dbl, P, i64, SP, vp])
+    _bind(L, "eik_peer_enable", [C.c_int32, C.c_int32])
     L.eik_last_error.restype = C.c_char_p
     L.eik_version.restype = C.c_char_p
     _lib = L
@@ -162,18 +174,20 @@ def _lib_f32():
     L = C.CDLL(LIB32)
     P, i64, dbl, vp = C.c_void_p, C.c_int64, C.c_double, C.c_void_p
     GP, SP = C.POINTER(Geom), C.POINTER(Stats)
-    L.eik_workspace_size_f32.argtypes = [GP, C.POINTER(C.c_size_t)]
-    L.eik_ifim_update_step_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]
-    L.eik_build_remedy_f32.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, SP, vp]
-    L.eik_remedy_load_f32.argtypes = [GP, P, P, P, C.c_size_t, C.POINTER(i64), vp]
-    L.eik_remedy_load_set_f32.argtypes = [GP, P, P, P, P, C.c_size_t, C.POINTER(i64), vp]
-    L.eik_remedy_export_f32.argtypes = [GP, P, C.c_size_t, P, vp]
-    L.eik_remedy_step_f32.argtypes = [GP, P, P, P, dbl, P, C.c_size_t, SP, vp]
-    L.eik_ifim_solve_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp]
-    L.eik_solve_fixpoint_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, i64, P, C.c_size_t, SP, vp]
-    L.eik_max_residual_f32.argtypes = [GP, P, P, P, P, C.c_size_t, C.POINTER(dbl), vp]
-    L.eik_solve_fim_f32.argtypes = [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, SP, vp]
-    L.eik_local_solve_f32.argtypes = [C.c_int, P, P, P, P, dbl, dbl, P, i64, vp]
+    _bind(L, "eik_workspace_size_f32", [GP, C.POINTER(C.c_size_t)])
+    _bind(L, "eik_ifim_update_step_f32", [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp])
+    _bind(L, "eik_build_remedy_f32", [GP, P, P, P, dbl, P, C.c_size_t, SP, vp])
+    _bind(L, "eik_remedy_load_f32", [GP, P, P, P, C.c_size_t, C.POINTER(i64), vp])
+    _bind(L, "eik_remedy_load_set_f32", [GP, P, P, P, P, C.c_size_t, C.POINTER(i64), vp])
+    _bind(L, "eik_field_max_diff_f32", [P, P, i64, P, C.POINTER(dbl), vp])
+    _bind(L, "eik_chunk_sha256_f32", [P, i64, i64, P, vp])
+    _bind(L, "eik_remedy_export_f32", [GP, P, C.c_size_t, P, vp])
+    _bind(L, "eik_remedy_step_f32", [GP, P, P, P, dbl, P, C.c_size_t, SP, vp])
+    _bind(L, "eik_ifim_solve_f32", [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, P, i64, SP, vp])
+    _bind(L, "eik_solve_fixpoint_f32", [GP, P, P, P, P, P, i64, dbl, i64, P, C.c_size_t, SP, vp])
+    _bind(L, "eik_max_residual_f32", [GP, P, P, P, P, C.c_size_t, C.POINTER(dbl), vp])
+    _bind(L, "eik_solve_fim_f32", [GP, P, P, P, P, P, i64, dbl, P, C.c_size_t, SP, vp])
+    _bind(L, "eik_local_solve_f32", [C.c_int, P, P, P, P, dbl, dbl, P, i64, vp])
     L.eik_last_error_f32.restype = C.c_char_p
     L.eik_version_f32.restype = C.c_char_p
     _lib32 = _Suffixed(L)

@@ -51,6 +51,8 @@
 
 #include "eik_ifim.h"
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: named ranges for nsys / ncu --nvtx
+
 // Field precision: float64 (parity mode, libeik_ifim.so) or float32 (perf mode,
 // libeik_ifim_f32.so: -DEIK_SINGLE=1, exported names carry the _f32 suffix).
 #ifndef EIK_SINGLE
@@ -215,6 +217,9 @@ struct KP {
 #endif
 #ifndef RT_MINB
 #define RT_MINB 4
+#endif
+#ifndef RT_ISO
+#define RT_ISO 1  // skip the solve of members whose neighbours did not change last round
 #endif
 constexpr int RT_GS = 32;  // grab counter stride (uint32): one 128-byte line per shard and slot
 enum { FS_SELF = 1, FS_XL = 2, FS_XH = 4, FS_YL = 8, FS_YH = 16, FS_ZL = 32, FS_ZH = 64 };
@@ -1251,6 +1256,106 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
     }
 }
 
+#ifndef REM_ASYNC
+#define REM_ASYNC 0  // 1: phase A gathers by cp.async into a per-warp double buffer (measured slower, PERF_LOG)
+#endif
+constexpr uint32_t NO_ENTRY = 0xffffffffu;
+
+// Asynchronous 4/8-byte global -> shared copy (L1-allocating), commit / wait on this thread's groups.
+__device__ __forceinline__ void cp_async(real_t *s, const real_t *g)
+{
+    const unsigned a = (unsigned)__cvta_generic_to_shared(s);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(a), "l"(g), "n"((int)sizeof(real_t)) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Issue the stencil copies of one member (list entry e, NO_ENTRY for none) into its lane's slots
+// sl[k * 32], k = c, w, e, s, n, d, u, coefficient; out-of-grid neighbours are +inf
+// (E/_kernels.py:21-38).  Returns row * 32W + x (its D word and bit), or NO_ENTRY.
+template <int DIM, int SOL>
+__device__ __forceinline__ uint32_t gather_async(const KP &p, const real_t *__restrict__ Pc, uint32_t e, real_t *sl)
+{
+    if (e == NO_ENTRY) return NO_ENTRY;
+    const uint32_t c = e & ~CARRY;
+    const uint32_t row = fdiv(c, p.fnx), x = c - row * p.nx32;
+    uint32_t y = row, z = 0;
+    if (DIM == 3) {
+        z = fdiv(row, p.fny);
+        y = row - z * (uint32_t)p.ny;
+    }
+    cp_async(sl, Pc + c);
+    if (x > 0) cp_async(sl + 32, Pc + (c - 1)); else sl[32] = INFINITY;
+    if (x + 1 < p.nx32) cp_async(sl + 64, Pc + (c + 1)); else sl[64] = INFINITY;
+    if (y > 0) cp_async(sl + 96, Pc + (c - p.nx32)); else sl[96] = INFINITY;
+    if (y + 1 < (uint32_t)p.ny) cp_async(sl + 128, Pc + (c + p.nx32)); else sl[128] = INFINITY;
+    if (DIM == 3) {
+        if (z > 0) cp_async(sl + 160, Pc + (c - p.plane32)); else sl[160] = INFINITY;
+        if (z + 1 < (uint32_t)p.nz) cp_async(sl + 192, Pc + (c + p.plane32)); else sl[192] = INFINITY;
+    }
+    cp_async(sl + 224, (SOL == SOL_A2 ? p.F : p.dd) + c);
+    return row * (p.W * 32u) + x;
+}
+
+// Phase A of one remedy round on a CTA's list segment [sbeg, mend): each warp relaxes 32
+// members per step while the copies of its next 32 are in flight.  Returns the decreases.
+template <int DIM, int SOL>
+__device__ __forceinline__ unsigned long long rem_phaseA_async(const KP &p, const uint32_t *__restrict__ ML,
+                                                               uint32_t sbeg, uint32_t mend,
+                                                               const real_t *__restrict__ Pc, real_t *__restrict__ Pn,
+                                                               uint32_t *Dc, real_t *stg)
+{
+    const unsigned lane = lane_id();
+    const uint32_t ws = WPB * 32;
+    const uint32_t wb = sbeg + (threadIdx.x >> 5) * 32;
+    unsigned long long a_dec = 0;
+    auto entry = [&](uint32_t i) { return i + lane < mend ? __ldcg(ML + i + lane) : NO_ENTRY; };
+    uint32_t ecur = entry(wb);
+    uint32_t pcur = gather_async<DIM, SOL>(p, Pc, ecur, stg + lane);
+    cp_async_commit();
+    uint32_t enext = entry(wb + ws);
+    uint32_t k = 0;
+    for (uint32_t i = wb; i < mend; i += ws, ++k) {
+        real_t *cur = stg + (k & 1) * 256 + lane;
+        const uint32_t pnext = gather_async<DIM, SOL>(p, Pc, enext, stg + ((k + 1) & 1) * 256 + lane);
+        cp_async_commit();
+        const uint32_t enn = entry(i + 2 * ws);
+        cp_async_wait<1>();  // this step's copies have landed
+        bool dec = false;
+        if (ecur != NO_ENTRY) {
+            Sten s;
+            s.c = cur[0]; s.w = cur[32]; s.e = cur[64]; s.s = cur[96]; s.n = cur[128];
+            s.d = DIM == 3 ? cur[160] : INFINITY;
+            s.u = DIM == 3 ? cur[192] : INFINITY;
+            s.k = cur[224];
+            const real_t v = solve<DIM, SOL>(p, s);
+            const uint32_t c = ecur & ~CARRY;
+            dec = v < s.c - tol_at(p.tol, s.c);  // E/ifim.py:203
+            if (dec) Pn[c] = v;
+            else if (ecur & CARRY) Pn[c] = s.c;  // changed last round: carry into the other buffer
+        }
+        // D_r bits: a warp's members of one word are contiguous in the list (segmented OR-scan,
+        // one atomicOr per word)
+        a_dec += __popc(__ballot_sync(FULL, dec));
+        const uint32_t wi = ecur != NO_ENTRY ? pcur >> 5 : 0xffffffffu;
+        uint32_t acc = dec ? (1u << (pcur & 31u)) : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t ov = __shfl_down_sync(FULL, acc, o);
+            const uint32_t ow = __shfl_down_sync(FULL, wi, o);
+            if (lane + o < 32 && ow == wi) acc |= ov;
+        }
+        const uint32_t pw = __shfl_up_sync(FULL, wi, 1);
+        if (acc && (lane == 0 || pw != wi)) atomicOr(Dc + wi, acc);
+        ecur = enext;
+        pcur = pnext;
+        enext = enn;
+    }
+    cp_async_wait<0>();
+    return a_dec;
+}
+
 #ifndef REM_MINB
 #define REM_MINB 4
 #endif
@@ -1259,6 +1364,7 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
 {
     __shared__ unsigned sscan[WPB + 1];
     __shared__ unsigned long long sred[WPB];
+    __shared__ real_t s_stage[(!MR && REM_ASYNC) ? WPB * 2 * 256 : 1];  // per warp: 2 steps x 8 values x 32 lanes
     if (skip && *skip) return;
     Ctl *ctl = p.ctl;
     const unsigned lane = lane_id();
@@ -1330,6 +1436,9 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
         const uint32_t seg = ((m + gnb - 1) / gnb + 32 * REM_MU - 1) / (32 * REM_MU) * (32 * REM_MU);
         const uint32_t sbeg = gb * seg, mend = min(m, sbeg + seg);
         const uint32_t wbase = sbeg + (threadIdx.x >> 5) * 32 * REM_MU, wstride = WPB * 32 * REM_MU;
+        if (!MR && REM_ASYNC)
+            a_dec = rem_phaseA_async<DIM, SOL>(p, ML, sbeg, mend, Pc, Pn, Dc, s_stage + (threadIdx.x >> 5) * 512);
+        else
         for (uint32_t i0 = wbase; i0 < mend; i0 += wstride) {
             uint32_t ent[REM_MU], rw[REM_MU], x[REM_MU];
             bool live[REM_MU];
@@ -1488,7 +1597,7 @@ __device__ __forceinline__ void rt_tile(const KP &p, uint32_t t, uint32_t r, uin
     const uint32_t yb = ty << G::LY, zb = tz << G::LZ;
     const uint32_t y = yb + ly, z = zb + lz;
     const uint32_t WNTY = p.W * p.nty;
-    uint32_t R, carry;
+    uint32_t R, carry, iso = 0;
     if (r == 0) {
         R = (y < ny && z < nz) ? __ldcg(p.R0b + (z * ny + y) * p.W + wx) : 0u;
         carry = 0;
@@ -1517,6 +1626,10 @@ __device__ __forceinline__ void rt_tile(const KP &p, uint32_t t, uint32_t r, uin
         }
         R = c | (dil & ~F);
         carry = c;
+        // members that decreased last round while none of their neighbours did: their inputs are
+        // the previous round's, so the solve returns their current value -- no decrease -- and
+        // only the carry write remains (the call is still counted)
+        iso = RT_ISO ? (c & ~dil) : 0u;
     }
     // members: warp scan of the row counts, expansion into the warp's shared list
     const uint32_t cnt = __popc(R);
@@ -1528,17 +1641,30 @@ __device__ __forceinline__ void rt_tile(const KP &p, uint32_t t, uint32_t r, uin
     }
     const uint32_t T = __shfl_sync(FULL, inc, 31);
     if (T == 0) return;
-    const uint32_t off = inc - cnt;
-    unsigned todo = __ballot_sync(FULL, R != 0);
+    // non-isolated members first, isolated ones (carry only) last
     const uint32_t lt = (1u << lane) - 1u;
-    while (todo) {
-        const int src = __ffs(todo) - 1;
-        todo &= todo - 1;
-        const uint32_t bits = __shfl_sync(FULL, R, src);
-        const uint32_t cb = __shfl_sync(FULL, carry, src);
-        const uint32_t o = __shfl_sync(FULL, off, src);
-        if ((bits >> lane) & 1u)
-            buf[o + __popc(bits & lt)] = (uint16_t)((((cb >> lane) & 1u) << 10) | ((uint32_t)src << 5) | lane);
+    const uint32_t Rs = R & ~iso, ns = __popc(Rs);
+    uint32_t is = ns;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_up_sync(FULL, is, o);
+        if (lane >= (unsigned)o) is += v;
+    }
+    const uint32_t T1 = __shfl_sync(FULL, is, 31);
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        const uint32_t Rp = pass ? iso : Rs;
+        const uint32_t off = pass ? T1 + (inc - cnt) - (is - ns) : is - ns;
+        unsigned todo = __ballot_sync(FULL, Rp != 0);
+        while (todo) {
+            const int src = __ffs(todo) - 1;
+            todo &= todo - 1;
+            const uint32_t bits = __shfl_sync(FULL, Rp, src);
+            const uint32_t cb = __shfl_sync(FULL, carry, src);
+            const uint32_t o = __shfl_sync(FULL, off, src);
+            if ((bits >> lane) & 1u)
+                buf[o + __popc(bits & lt)] = (uint16_t)((((cb >> lane) & 1u) << 10) | ((uint32_t)src << 5) | lane);
+        }
     }
     sD[lane] = 0;
     __syncwarp();
@@ -1551,6 +1677,10 @@ __device__ __forceinline__ void rt_tile(const KP &p, uint32_t t, uint32_t r, uin
         const uint32_t row = (e >> 5) & 31u, bit = e & 31u;
         const uint32_t x = x0 + bit, yy = yb + (row & (G::TY - 1)), zz = zb + (row >> G::LY);
         const uint32_t c = DIM == 3 ? (zz * ny + yy) * nx + x : yy * nx + x;
+        if (b >= T1) {  // isolated members only: carry the value over
+            if (live) Pn[c] = __ldca(Pc + c);
+            continue;
+        }
         Sten s;
         s.c = s.w = s.e = s.s = s.n = s.d = s.u = INFINITY;
         s.k = R_ONE;
@@ -2049,10 +2179,143 @@ __global__ void k_local(int kind, const real_t *a, const real_t *b, const real_t
 }
 
 // ---------------------------------------------------------------------------
+// Verification reductions on device fields (E/harness.py:165-179, SURVEY.md
+// §8f rank 2): no full-field host copy at 512^3-1024^3.
+//   k_max_diff   max |a - b| with equal same-sign infinities counting 0 and NaN
+//                propagating (np.where(both_inf, 0, |a - b|).max())
+//   k_sha256_chunks  SHA-256 of each `chunk`-byte piece of a byte range (one thread per
+//                piece, FIPS 180-4); the host hashes the concatenated piece digests.
+// ---------------------------------------------------------------------------
+__global__ void k_max_diff(const real_t *__restrict__ a, const real_t *__restrict__ b, int64_t n,
+                           unsigned long long *out)
+{
+    unsigned long long m = 0;
+    unsigned nan = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const real_t x = __ldcs(a + i), y = __ldcs(b + i);
+        if (isinf(x) && isinf(y) && ((x > R_ZERO) == (y > R_ZERO))) continue;  // both_inf: 0
+        const real_t d = fabs(x - y);
+        if (!(d == d)) {
+            nan = 1;
+            continue;
+        }
+        const unsigned long long bb = bits_of(d);
+        m = bb > m ? bb : m;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long t = __shfl_xor_sync(FULL, m, o);
+        m = t > m ? t : m;
+    }
+    nan = __any_sync(FULL, nan);
+    if (lane_id() == 0) {
+        if (m) atomicMax(out, m);
+        if (nan) atomicOr(out + 1, 1ull);
+    }
+}
+
+__constant__ uint32_t kSha256K[64] = {
+    0x428a2f98u, 0x71374491u, 0xb5c0fbcfu, 0xe9b5dba5u, 0x3956c25bu, 0x59f111f1u, 0x923f82a4u, 0xab1c5ed5u,
+    0xd807aa98u, 0x12835b01u, 0x243185beu, 0x550c7dc3u, 0x72be5d74u, 0x80deb1feu, 0x9bdc06a7u, 0xc19bf174u,
+    0xe49b69c1u, 0xefbe4786u, 0x0fc19dc6u, 0x240ca1ccu, 0x2de92c6fu, 0x4a7484aau, 0x5cb0a9dcu, 0x76f988dau,
+    0x983e5152u, 0xa831c66du, 0xb00327c8u, 0xbf597fc7u, 0xc6e00bf3u, 0xd5a79147u, 0x06ca6351u, 0x14292967u,
+    0x27b70a85u, 0x2e1b2138u, 0x4d2c6dfcu, 0x53380d13u, 0x650a7354u, 0x766a0abbu, 0x81c2c92eu, 0x92722c85u,
+    0xa2bfe8a1u, 0xa81a664bu, 0xc24b8b70u, 0xc76c51a3u, 0xd192e819u, 0xd6990624u, 0xf40e3585u, 0x106aa070u,
+    0x19a4c116u, 0x1e376c08u, 0x2748774cu, 0x34b0bcb5u, 0x391c0cb3u, 0x4ed8aa4au, 0x5b9cca4fu, 0x682e6ff3u,
+    0x748f82eeu, 0x78a5636fu, 0x84c87814u, 0x8cc70208u, 0x90befffau, 0xa4506cebu, 0xbef9a3f7u, 0xc67178f2u};
+
+__device__ __forceinline__ uint32_t rotr32(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+
+__device__ void sha256_block(uint32_t h[8], uint32_t w[16])
+{
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], k = h[7];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+        uint32_t wi;
+        if (i < 16) {
+            wi = w[i];
+        } else {
+            const uint32_t w15 = w[(i - 15) & 15], w2 = w[(i - 2) & 15];
+            const uint32_t s0 = rotr32(w15, 7) ^ rotr32(w15, 18) ^ (w15 >> 3);
+            const uint32_t s1 = rotr32(w2, 17) ^ rotr32(w2, 19) ^ (w2 >> 10);
+            wi = w[i & 15] = w[i & 15] + s0 + w[(i - 7) & 15] + s1;
+        }
+        const uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t t1 = k + S1 + ch + kSha256K[i] + wi;
+        const uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        const uint32_t t2 = S0 + mj;
+        k = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += k;
+}
+
+__global__ void k_sha256_chunks(const uint8_t *__restrict__ data, uint64_t nbytes, uint64_t chunk, uint64_t nchunks,
+                                uint8_t *__restrict__ dig)
+{
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= nchunks) return;
+    const uint8_t *p = data + i * chunk;
+    const uint64_t len = min(chunk, nbytes - i * chunk);
+    uint32_t h[8] = {0x6a09e667u, 0xbb67ae85u, 0x3c6ef372u, 0xa54ff53au,
+                     0x510e527fu, 0x9b05688cu, 0x1f83d9abu, 0x5be0cd19u};
+    uint32_t w[16];
+    const uint64_t nfull = len / 64;
+    for (uint64_t blk = 0; blk < nfull; ++blk) {
+        const uint4 *q = (const uint4 *)(p + blk * 64);  // chunk and base are 16-byte aligned
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const uint4 x = __ldcs(q + v);
+            w[4 * v + 0] = __byte_perm(x.x, 0, 0x0123);
+            w[4 * v + 1] = __byte_perm(x.y, 0, 0x0123);
+            w[4 * v + 2] = __byte_perm(x.z, 0, 0x0123);
+            w[4 * v + 3] = __byte_perm(x.w, 0, 0x0123);
+        }
+        sha256_block(h, w);
+    }
+    // tail: the remaining bytes, 0x80, zeros, 64-bit big-endian bit length (one or two blocks)
+    const uint32_t rem = (uint32_t)(len - nfull * 64);
+    const uint8_t *t = p + nfull * 64;
+    const uint64_t bits = len * 8;
+    const int nblk = rem + 9 <= 64 ? 1 : 2;
+    for (int bk = 0; bk < nblk; ++bk) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            uint32_t word = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t pos = (uint32_t)(bk * 64 + 4 * j + q);
+                uint32_t byte = 0;
+                if (pos < rem) byte = t[pos];
+                else if (pos == rem) byte = 0x80u;
+                else if (bk == nblk - 1 && 4 * j + q >= 56) byte = (uint32_t)(bits >> (8 * (63 - (4 * j + q)))) & 0xffu;
+                word = (word << 8) | byte;
+            }
+            w[j] = word;
+        }
+        sha256_block(h, w);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        dig[32 * i + 4 * j + 0] = (uint8_t)(h[j] >> 24);
+        dig[32 * i + 4 * j + 1] = (uint8_t)(h[j] >> 16);
+        dig[32 * i + 4 * j + 2] = (uint8_t)(h[j] >> 8);
+        dig[32 * i + 4 * j + 3] = (uint8_t)h[j];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
 
 thread_local std::string g_err;
+
+// NVTX range over a scope (host side: the enqueue of a phase's kernels; SURVEY.md §5 tracing)
+struct Nvtx {
+    explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
 
 int fail(int code, const char *fmt, ...)
 {
@@ -2501,6 +2764,7 @@ int EIK_FN(eik_ifim_update_step)(const eik_geom *g, real_t *phi, const real_t *s
     if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
     if (nseeds < 1 || !seed_idx || !seed_val) return fail(EIK_EINVAL, "boundary condition has no seeds");
     cudaStream_t st = (cudaStream_t)stream;
+    Nvtx nvtx_range("eik update step (E/ifim.py:75-134)");
     memset(out, 0, sizeof(*out));
     Events ev;
     ev.rec(0, st);
@@ -2540,6 +2804,7 @@ int EIK_FN(eik_build_remedy)(const eik_geom *g, const real_t *phi, const real_t 
     if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
     if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
     cudaStream_t st = (cudaStream_t)stream;
+    Nvtx nvtx_range("eik build pass (E/ifim.py:137-161)");
     memset(out, 0, sizeof(*out));
     char *b = (char *)workspace;
     Ctl *ctl = (Ctl *)(b + L.off_ctl_r);
@@ -2621,6 +2886,7 @@ int EIK_FN(eik_remedy_step)(const eik_geom *g, real_t *phi, const real_t *speed,
     if (!(tol > 0)) return fail(EIK_EINVAL, "tol must be positive, got %g", tol);
     if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
     cudaStream_t st = (cudaStream_t)stream;
+    Nvtx nvtx_range("eik remedy step (E/ifim.py:164-218)");
     memset(out, 0, sizeof(*out));
     char *b = (char *)workspace;
     Ctl *ctl = (Ctl *)(b + L.off_ctl_r);
@@ -2673,8 +2939,12 @@ int EIK_FN(eik_ifim_solve)(const eik_geom *g, real_t *phi, const real_t *speed, 
     Ctl *cr = (Ctl *)(b + L.off_ctl_r);
     Events ev;
     int64_t launches = 0;
+    Nvtx range_solve("eik_ifim_solve");
     ev.rec(0, st);
-    rc = run_update(g, L, phi, speed, state, seed_idx, seed_val, nseeds, tol, workspace, st, launches);
+    {
+        Nvtx r("eik update step (E/ifim.py:75-134)");
+        rc = run_update(g, L, phi, speed, state, seed_idx, seed_val, nseeds, tol, workspace, st, launches);
+    }
     if (rc) return rc;
     ev.rec(1, st);
     KP p = make_kp(g, L, workspace, phi, speed, state, tol, cr, L.cap_rem);
@@ -2682,10 +2952,16 @@ int EIK_FN(eik_ifim_solve)(const eik_geom *g, real_t *phi, const real_t *speed, 
     // changed in the last-but-one iteration rewrote itself in the last one),
     // so the build reads the caller's buffer and the remedy starts at parity 0.
     const unsigned *skip = &cu->err;
-    rc = dispatch(g, [&](auto E) { return E.build(p, phi, skip, st); });
+    {
+        Nvtx r("eik build pass (E/ifim.py:137-161)");
+        rc = dispatch(g, [&](auto E) { return E.build(p, phi, skip, st); });
+    }
     if (rc) return rc;
     ev.rec(2, st);
-    rc = dispatch(g, [&](auto E) { return E.remedy_single(p, skip, st); });
+    {
+        Nvtx r("eik remedy step (E/ifim.py:164-218)");
+        rc = dispatch(g, [&](auto E) { return E.remedy_single(p, skip, st); });
+    }
     if (rc) return rc;
     ev.rec(3, st);
     launches += 2;
@@ -2751,6 +3027,7 @@ int EIK_FN(eik_solve_fixpoint)(const eik_geom *g, real_t *phi, const real_t *spe
     if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
     if (nseeds < 1 || !seed_idx || !seed_val) return fail(EIK_EINVAL, "boundary condition has no seeds");
     cudaStream_t st = (cudaStream_t)stream;
+    Nvtx nvtx_range("eik fixpoint (E/oracle.py:22-70)");
     memset(out, 0, sizeof(*out));
     char *b = (char *)workspace;
     Ctl *ctl = (Ctl *)(b + L.off_ctl_r);
@@ -2806,6 +3083,7 @@ int EIK_FN(eik_solve_fim)(const eik_geom *g, real_t *phi, const real_t *speed, u
     if (!phi || !speed || !state || !out) return fail(EIK_EINVAL, "null array");
     if (nseeds < 1 || !seed_idx || !seed_val) return fail(EIK_EINVAL, "boundary condition has no seeds");
     cudaStream_t st = (cudaStream_t)stream;
+    Nvtx nvtx_range("eik FIM (E/fim.py:62-144)");
     memset(out, 0, sizeof(*out));
     char *b = (char *)workspace;
     Ctl *ctl = (Ctl *)(b + L.off_ctl_u);
@@ -2997,6 +3275,7 @@ int eik_mr_run(const eik_geom *g, int32_t R, const eik_rank *ranks, int32_t r_be
     if (r_begin < 0 || r_end > R || r_begin >= r_end) return fail(EIK_EINVAL, "bad local rank range");
     if (!out) return fail(EIK_EINVAL, "null stats");
     cudaStream_t st = (cudaStream_t)stream;
+    Nvtx nvtx_range("eik multi-rank solve");
     memset(out, 0, sizeof(*out));
     const int nl = r_end - r_begin;
     Events ev;
@@ -3245,6 +3524,54 @@ int eik_slab_remedy_round(const eik_geom *g, real_t *phi, const real_t *speed, c
 }
 
 #endif  // !EIK_SINGLE
+
+int EIK_FN(eik_field_max_diff)(const real_t *a, const real_t *b, int64_t n, void *scratch, double *out, void *stream)
+{
+    if (!out) return fail(EIK_EINVAL, "null output");
+    if (n < 0 || (n > 0 && (!a || !b || !scratch))) return fail(EIK_EINVAL, "null array");
+    if (n == 0) {  // E/harness.py:170-171
+        *out = 0.0;
+        return EIK_OK;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    unsigned long long *acc = (unsigned long long *)scratch;
+    CK(cudaMemsetAsync(acc, 0, 16, st));
+    k_max_diff<<<stream_grid((n + 31) / 32), BLOCK, 0, st>>>(a, b, n, acc);
+    CK(cudaGetLastError());
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, acc, 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (h[1]) {
+        *out = NAN;
+    } else {
+#if EIK_SINGLE
+        const unsigned b32 = (unsigned)h[0];
+        float f;
+        memcpy(&f, &b32, 4);
+        *out = (double)f;
+#else
+        double d;
+        memcpy(&d, &h[0], 8);
+        *out = d;
+#endif
+    }
+    return EIK_OK;
+}
+
+int EIK_FN(eik_chunk_sha256)(const void *data, int64_t nbytes, int64_t chunk, uint8_t *digests, void *stream)
+{
+    if (nbytes < 0 || chunk < 64 || (chunk & 63)) return fail(EIK_EINVAL, "chunk must be a positive multiple of 64 bytes");
+    if (nbytes > 0 && (!data || !digests)) return fail(EIK_EINVAL, "null array");
+    if ((uintptr_t)data & 15) return fail(EIK_EINVAL, "data must be 16-byte aligned");
+    const uint64_t nch = nbytes ? ((uint64_t)nbytes + chunk - 1) / chunk : 0;
+    if (!nch) return EIK_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    k_sha256_chunks<<<(unsigned)((nch + 127) / 128), 128, 0, st>>>((const uint8_t *)data, (uint64_t)nbytes,
+                                                                   (uint64_t)chunk, nch, digests);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return EIK_OK;
+}
 
 int EIK_FN(eik_local_solve)(int kind, const real_t *a, const real_t *b, const real_t *c, const real_t *f, double dx,
                     double dy, real_t *out, int64_t n, void *stream)

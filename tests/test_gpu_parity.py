@@ -3,6 +3,7 @@ from the live reference and against the CPU oracle.  Bit-exact float64 phi and
 equal RunStats integers (iterations, solver_calls, peak_active, peak_remedy,
 active_history) are required everywhere."""
 import hashlib
+import os
 
 import numpy as np
 import pytest
@@ -15,6 +16,7 @@ from oracle import cpu
 pytestmark = pytest.mark.gpu
 
 DEV = torch.device("cuda:0")
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 
 
 def sha(a):
