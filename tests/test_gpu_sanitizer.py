@@ -9,7 +9,10 @@ import sys
 
 import pytest
 
-pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+pytestmark = [pytest.mark.gpu, pytest.mark.slow,
+              pytest.mark.skipif(os.environ.get("EIK_SANITIZER") != "1",
+                                 reason="compute-sanitizer is closed on the gpurun pool (runs under it left "
+                                        "GPUs needing a reset); opt in with EIK_SANITIZER=1 on a box that allows it")]
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SAN = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
 
