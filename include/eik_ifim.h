@@ -206,6 +206,10 @@ int eik_peer_enable(int32_t device, int32_t peer);
 
 const char *eik_last_error(void);
 const char *eik_version(void);
+/* Which engine ran the calling thread's last remedy step: 0 none, 1 member list (k_remedy),
+ * 2 tile (k_remedy_t), 3 TMA brick pipeline (k_remedy_b).  Selection: EIK_REMEDY=list|tile|brick,
+ * else the default (3D single device: brick when eligible). */
+int eik_last_remedy_engine(void);
 
 /* ---- float32 perf mode (libeik_ifim_f32.so) ----
  * Same semantics and statistics definitions with float32 phi / speed (geometry
@@ -243,6 +247,7 @@ int eik_local_solve_f32(int kind, const float *a, const float *b, const float *c
                         double dy, float *out, int64_t n, void *stream);
 const char *eik_last_error_f32(void);
 const char *eik_version_f32(void);
+int eik_last_remedy_engine_f32(void);
 
 #ifdef __cplusplus
 }

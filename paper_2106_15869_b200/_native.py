@@ -14,6 +14,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 SRC = os.path.join(HERE, "csrc", "eik_ifim.cu")
+DEPS = [os.path.join(HERE, "csrc", f) for f in ("eik_remedy_tma.cuh",)]
 HDR = os.path.join(ROOT, "include", "eik_ifim.h")
 LIB = os.path.join(HERE, "libeik_ifim.so")
 LIB32 = os.path.join(HERE, "libeik_ifim_f32.so")  # float32 perf mode (-DEIK_SINGLE=1, names suffixed _f32)
@@ -33,7 +34,7 @@ EXPORTS = (
     "eik_workspace_size", "eik_ifim_update_step", "eik_build_remedy", "eik_remedy_load", "eik_remedy_load_set",
     "eik_field_max_diff", "eik_chunk_sha256",
     "eik_remedy_export", "eik_remedy_step", "eik_ifim_solve", "eik_local_solve",
-    "eik_last_error", "eik_version", "eik_workspace_offsets", "eik_slab_update_init", "eik_slab_update_iter",
+    "eik_last_error", "eik_version", "eik_last_remedy_engine", "eik_workspace_offsets", "eik_slab_update_init", "eik_slab_update_iter",
     "eik_slab_apply_requests", "eik_slab_build", "eik_slab_remedy_round", "eik_solve_fixpoint",
     "eik_max_residual", "eik_mr_prepare", "eik_mr_run", "eik_peer_enable", "eik_solve_fim",
 )
@@ -49,7 +50,7 @@ def nvcc() -> str:
 def build(force: bool = False, verbose: bool = False) -> str:
     """Compile csrc/eik_ifim.cu into paper_2106_15869_b200/libeik_ifim.so (float64) and
     libeik_ifim_f32.so (float32 perf mode)."""
-    src_t = max(os.path.getmtime(SRC), os.path.getmtime(HDR))
+    src_t = max(os.path.getmtime(f) for f in (SRC, HDR, *DEPS))
     for out, extra in ((LIB, []), (LIB32, ["-DEIK_SINGLE=1"])):
         if force or not os.path.exists(out) or os.path.getmtime(out) < src_t:
             cmd = [nvcc(), *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-o", out + ".tmp", SRC]
@@ -94,6 +95,7 @@ EXPORTS_F32 = (
     "eik_remedy_load_set_f32", "eik_field_max_diff_f32", "eik_chunk_sha256_f32",
     "eik_remedy_export_f32", "eik_remedy_step_f32", "eik_ifim_solve_f32", "eik_solve_fixpoint_f32",
     "eik_max_residual_f32", "eik_local_solve_f32", "eik_last_error_f32", "eik_version_f32", "eik_solve_fim_f32",
+    "eik_last_remedy_engine_f32",
 )
 
 _lib = None
@@ -192,6 +194,15 @@ def _lib_f32():
     L.eik_version_f32.restype = C.c_char_p
     _lib32 = _Suffixed(L)
     return _lib32
+
+
+REMEDY_ENGINES = {0: "none", 1: "list", 2: "tile", 3: "brick"}
+
+
+def last_remedy_engine(dtype: int = EIK_F64) -> str:
+    """Engine of this thread's last remedy step (list / tile / brick, eik_last_remedy_engine)."""
+    L = lib(dtype)
+    return REMEDY_ENGINES[int((L.eik_last_remedy_engine_f32 if dtype == EIK_F32 else L.eik_last_remedy_engine)())]
 
 
 def check(rc: int, dtype: int | None = None) -> None:

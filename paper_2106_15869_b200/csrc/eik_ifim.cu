@@ -36,6 +36,8 @@
 // launch, 10 s watchdog) and read the global set size after each barrier;
 // the host sees only the final statistics.
 
+#include <cuda.h>          // CUtensorMap (TMA descriptors)
+#include <cudaTypedefs.h>  // PFN_cuTensorMapEncodeTiled
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -196,6 +198,15 @@ struct KP {
     uint32_t *Dt0, *Dt1;         // D_r, tile-major, by round parity
     uint32_t *stamp0, *stamp1;   // per tile: (round + 1) << 7 | faces of its D_r line, by round parity
     unsigned *grab;              // [3 slots][RT_SHARDS] chunk counters, one 128-byte line each
+    // remedy brick engine (k_remedy_b, single device 3D; eik_remedy_tma.cuh): 32 x 8 x 8 bricks,
+    // brick-major D records by round parity, fixed words, per-round masks and brick lists
+    uint32_t nbx, nby, nbz, nbricks;
+    FastDiv fnbx, fnby;
+    uint32_t *brec0, *brec1;     // [nbricks][128 words]: own D rows + face summaries
+    uint32_t *bfix;              // [nbricks][64 words]: fixed rows (outside the grid: all ones)
+    uint32_t *bmask;             // [3 slots][nbricks]: which records a brick reads next round
+    uint32_t *blist0, *blist1;   // [nbricks]: active bricks of a round, by parity
+    unsigned *bcnt;              // [3 slots] list lengths, [3 slots] grab counters (128-byte lines)
     // multi-rank (peer slabs): this rank owns planes [zg0, zg0 + nz) of the global grid
     int32_t mr, q, R, pad2;
     uint32_t gb0, gnb;     // this rank's CTAs: blockIdx.x in [gb0, gb0 + gnb)
@@ -208,6 +219,9 @@ struct KP {
 // Remedy tile engine geometry (k_remedy_t below)
 #ifndef REMEDY_TILE_DEFAULT
 #define REMEDY_TILE_DEFAULT 0  // single-device remedy: 1 = tile engine, 0 = member-list kernel
+#endif
+#ifndef REMEDY_BRICK_DEFAULT
+#define REMEDY_BRICK_DEFAULT 0  // single-device 3D remedy: 1 = brick engine (TMA), 0 = as below
 #endif
 #ifndef RT_SHARDS
 #define RT_SHARDS 32
@@ -1842,6 +1856,8 @@ __global__ void __launch_bounds__(BLOCK, RT_MINB) k_remedy_t(KP p, const unsigne
     }
 }
 
+#include "eik_remedy_tma.cuh"
+
 // ---------------------------------------------------------------------------
 // Fixpoint reference (E/oracle.py:22-70): full-grid Jacobi passes
 // phi <- min(phi, U(snapshot)) over every free cell until nothing decreases or
@@ -2310,6 +2326,7 @@ __global__ void k_sha256_chunks(const uint8_t *__restrict__ data, uint64_t nbyte
 // ---------------------------------------------------------------------------
 
 thread_local std::string g_err;
+thread_local int g_remedy_engine = 0;  // eik_last_remedy_engine()
 
 // NVTX range over a scope (host side: the enqueue of a phase's kernels; SURVEY.md §5 tracing)
 struct Nvtx {
@@ -2344,6 +2361,8 @@ struct Layout {
     size_t off_hist, off_ctl_u, off_ctl_r, off_kps, total;
     size_t off_ft, off_sb, off_dt0, off_dt1, off_st0, off_st1, off_grab;  // remedy tile engine
     uint32_t tnty, tntz, ntiles;
+    size_t off_brec0, off_brec1, off_bfix, off_bmask, off_blist0, off_blist1, off_bcnt;  // brick engine
+    uint32_t nbx, nby, nbz, nbricks;
     int64_t cap_upd, cap_rem;
 };
 
@@ -2403,6 +2422,21 @@ int make_layout(const eik_geom *g, Layout &L)
         L.off_st0 = o; o += al((size_t)nt * 4);
         L.off_st1 = o; o += al((size_t)nt * 4);
         L.off_grab = o; o += al((size_t)3 * 32 * RT_GS * 4);
+    }
+    // remedy brick engine (3D): 32 x 8 x 8 bricks
+    {
+        L.nbx = (uint32_t)W;
+        L.nby = (uint32_t)((g->ny + 7) / 8);
+        L.nbz = g->ndim == 3 ? (uint32_t)((g->nz + 7) / 8) : 1u;
+        L.nbricks = L.nbx * L.nby * L.nbz;
+        const size_t nb = L.nbricks;
+        L.off_brec0 = o; o += al(nb * 512);
+        L.off_brec1 = o; o += al(nb * 512);
+        L.off_bfix = o; o += al(nb * 256);
+        L.off_bmask = o; o += al(3 * nb * 4);
+        L.off_blist0 = o; o += al(nb * 4);
+        L.off_blist1 = o; o += al(nb * 4);
+        L.off_bcnt = o; o += al(6 * 128);
     }
     // member-list traversal (word_at): 3D groups of 4x4 rows, 2D groups of 16 rows, per x-word
     if (g->ndim == 3) {
@@ -2475,6 +2509,16 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, real_t *phi, const real
     p.stamp0 = (uint32_t *)(b + L.off_st0);
     p.stamp1 = (uint32_t *)(b + L.off_st1);
     p.grab = (unsigned *)(b + L.off_grab);
+    p.nbx = L.nbx; p.nby = L.nby; p.nbz = L.nbz; p.nbricks = L.nbricks;
+    p.fnbx = make_fastdiv(L.nbx);
+    p.fnby = make_fastdiv(L.nby);
+    p.brec0 = (uint32_t *)(b + L.off_brec0);
+    p.brec1 = (uint32_t *)(b + L.off_brec1);
+    p.bfix = (uint32_t *)(b + L.off_bfix);
+    p.bmask = (uint32_t *)(b + L.off_bmask);
+    p.blist0 = (uint32_t *)(b + L.off_blist0);
+    p.blist1 = (uint32_t *)(b + L.off_blist1);
+    p.bcnt = (unsigned *)(b + L.off_bcnt);
     return p;
 }
 
@@ -2539,6 +2583,38 @@ int coop_launch_groups(K kernel, const KP *kps_dev, int nlocal, cudaStream_t st,
     e = cudaLaunchCooperativeKernel((const void *)kernel, grid, block, args, 0, st);
     if (e != cudaSuccess) return fail(EIK_ECUDA, "cooperative launch: %s", cudaGetErrorString(e));
     return EIK_OK;
+}
+
+// TMA descriptors (cuTensorMapEncodeTiled through the runtime's driver entry point: no -lcuda)
+int encode_3d(CUtensorMap *tm, CUtensorMapDataType dt, size_t esz, const void *base, uint64_t nx, uint64_t ny,
+              uint64_t nz, uint32_t bx, uint32_t by, uint32_t bz)
+{
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !f)
+            return fail(EIK_ECUDA, "cuTensorMapEncodeTiled is not available");
+        fn = (PFN_cuTensorMapEncodeTiled_v12000)f;
+    }
+    const cuuint64_t dims[3] = {nx, ny, nz};
+    const cuuint64_t strides[2] = {nx * esz, nx * ny * esz};
+    const cuuint32_t box[3] = {bx, by, bz}, es[3] = {1, 1, 1};
+    const CUresult r = fn(tm, dt, 3, const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(EIK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return EIK_OK;
+}
+
+// The brick engine needs TMA-legal strides (16-byte multiples), a box no larger than the grid
+// and 16-byte-aligned fields.
+bool brick_eligible(const KP &p)
+{
+    const uint64_t rowb = (uint64_t)p.nx32 * sizeof(real_t);
+    return !p.mr && !p.slab && p.nz > 1 && rowb % 16 == 0 && p.nx32 >= (uint32_t)brk::HX && p.ny >= brk::HY &&
+           p.nz >= brk::HZ && ((uintptr_t)p.P0 & 15) == 0 && ((uintptr_t)p.P1 & 15) == 0 && ((uintptr_t)p.dd & 15) == 0;
 }
 
 template <int DIM, int SOL>
@@ -2628,10 +2704,45 @@ struct Engine {
     }
     // single device: EIK_REMEDY=list (member-list kernel) or tile (tile engine); hand-built sets
     // with members outside their work list need the tile engine
+    // brick engine (eik_remedy_tma.cuh): TMA-staged bricks, 3D single device
+    static int remedy_brick(KP &p, const unsigned *skip, cudaStream_t st)
+    {
+        const CUtensorMapDataType dt = sizeof(real_t) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+        CUtensorMap m0, m1, md;
+        int rc = encode_3d(&m0, dt, sizeof(real_t), p.P0, p.nx32, p.ny, p.nz, brk::HX, brk::HY, brk::HZ);
+        if (!rc) rc = encode_3d(&m1, dt, sizeof(real_t), p.P1, p.nx32, p.ny, p.nz, brk::HX, brk::HY, brk::HZ);
+        if (!rc) rc = encode_3d(&md, dt, sizeof(real_t), p.dd, p.nx32, p.ny, p.nz, brk::BX, brk::BY, brk::BZ);
+        if (rc) return rc;
+        CK(cudaMemsetAsync(p.bmask, 0, (size_t)3 * p.nbricks * 4, st));
+        CK(cudaMemsetAsync(p.bcnt, 0, 6 * 128, st));
+        k_brick_prep<<<stream_grid((int64_t)p.nbricks), 256, 0, st>>>(p);
+        CK(cudaGetLastError());
+        auto kern = k_remedy_b<SOL>;
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)brk::SMEM));
+        int occ = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, brk::THREADS, brk::SMEM));
+        if (const char *env = getenv("EIK_BRK_BLOCKS_PER_SM")) {
+            const int v = atoi(env);
+            if (v > 0 && v <= occ) occ = v;
+        }
+        if (occ < 1) return fail(EIK_ECUDA, "brick remedy kernel cannot be resident");
+        dim3 grid(occ * num_sms()), block(brk::THREADS);
+        void *args[] = {&p, (void *)&skip, &m0, &m1, &md};
+        const cudaError_t e = cudaLaunchCooperativeKernel((const void *)kern, grid, block, args, brk::SMEM, st);
+        if (e != cudaSuccess) return fail(EIK_ECUDA, "cooperative launch (brick remedy): %s", cudaGetErrorString(e));
+        return EIK_OK;
+    }
     static int remedy_single(KP &p, const unsigned *skip, cudaStream_t st, bool need_tile = false)
     {
         const char *mode = getenv("EIK_REMEDY");
-        const bool tile = need_tile || (mode ? strcmp(mode, "list") != 0 : REMEDY_TILE_DEFAULT);
+        if constexpr (DIM == 3 && SOL == SOL_U3) {
+            if (!need_tile && brick_eligible(p) && (mode ? strcmp(mode, "brick") == 0 : REMEDY_BRICK_DEFAULT)) {
+                g_remedy_engine = 3;
+                return remedy_brick(p, skip, st);
+            }
+        }
+        const bool tile = need_tile || (mode ? strcmp(mode, "tile") == 0 : REMEDY_TILE_DEFAULT);
+        g_remedy_engine = tile ? 2 : 1;
         if (!tile) return remedy(p, skip, st);
         CK(cudaMemsetAsync(p.stamp0, 0, (size_t)p.ntiles * 4, st));
         CK(cudaMemsetAsync(p.stamp1, 0, (size_t)p.ntiles * 4, st));
@@ -2731,6 +2842,7 @@ int expose_latest(const Layout &L, const Ctl &c, real_t *phi, const real_t *phi2
 extern "C" {
 
 const char *EIK_FN(eik_last_error)(void) { return g_err.c_str(); }
+int EIK_FN(eik_last_remedy_engine)(void) { return g_remedy_engine; }
 
 const char *EIK_FN(eik_version)(void)
 {
