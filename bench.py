@@ -202,15 +202,15 @@ def hbm_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def traffic_from_profiles(workload: str):
-    """dram bytes per launch of k_remedy from the committed ncu --set full summary, if any."""
+def traffic_from_profiles(workload: str, kernel: str = "k_remedy"):
+    """dram bytes per launch of the remedy kernel from the committed ncu --set full summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        e = d.get("kernels", {}).get("k_remedy", {})
-        if e.get("workload") == workload:
-            return float(e["dram_bytes_read"]) + float(e["dram_bytes_write"])
+        for e in (d.get("kernels", {}).get(kernel, {}), *d.get("captures", {}).get(kernel, [])):
+            if e.get("workload") == workload:
+                return float(e["dram_bytes_read"]) + float(e["dram_bytes_write"])
     except Exception:
         pass
     return None
@@ -712,6 +712,11 @@ def run_ours(args):
     for _ in range(args.warmup):
         r = step()
     torch.cuda.synchronize()
+    from paper_2106_15869_b200 import _native as _nat
+
+    # which remedy engine ran (member list / TMA brick pipeline, chosen on the device from |R_0|)
+    remedy_engine = _nat.last_remedy_engine(_nat.EIK_F32 if args.dtype == "f32" else _nat.EIK_F64) \
+        if mode == "single" and args.method == "ifim" else ("list (peer slabs)" if mode != "single" else None)
     calls = r.calls
     stream = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -752,7 +757,9 @@ def run_ours(args):
     if mode == "peer":
         peak, peak_src = peak * world, peak_src + f" x {world} ranks"
     achieved = alg_bytes / rem_s / 1e9 if rem_s > 0 else None
-    traffic = traffic_from_profiles(workload) if not slabs and args.dtype == "f64" and args.method == "ifim" else None
+    rem_kernel = "k_fim" if args.method == "fim" else ("k_remedy_b" if remedy_engine == "brick" else "k_remedy")
+    traffic = traffic_from_profiles(workload, rem_kernel) if not slabs and args.dtype == "f64" and args.method == "ifim" \
+        else None
 
     parity, parity_detail = parity_vs_oracle(torch, w, r, world, rank, args.dtype) if args.method == "ifim" \
         else ("not-checked", "FIM baseline (bit-exact vs the oracle in tests/test_gpu_fim.py)")
@@ -780,7 +787,7 @@ def run_ours(args):
             "scaling": "strong" if slabs else "weak",
             "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": workload, "size": n, "method": args.method, "solver_calls_per_step": calls,
-                       "iterations": r.iterations, "peak_remedy": r.peak_remedy,
+                       "iterations": r.iterations, "peak_remedy": r.peak_remedy, "remedy_engine": remedy_engine,
                        "parallelism": {"peer": f"z-slabs x{world} (peer-memory fused kernels)",
                                        "host": f"z-slabs x{world} (host-driven exchange)"}.get(mode, "single"),
                        "l2": (f"inputs larger than L2 (phi {w.cells * 8 / 2 ** 30:g} GiB fp64 per field)"
@@ -791,7 +798,7 @@ def run_ours(args):
             "grid_cells_per_s": w.cells / (ms / args.steps * 1e-3),  # N / wall
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "k_fim" if args.method == "fim" else "k_remedy", "alg_bytes_per_launch": alg_bytes,
+                         "kernel": rem_kernel, "alg_bytes_per_launch": alg_bytes,
                          "launch_ms": rem_s * 1e3,
                          "peak_source": peak_src},
             "phase_roofline": ({k: round(b / (r.phase_ms[k] * 1e-3) / 1e9 / hbm_peak()[0], 4)

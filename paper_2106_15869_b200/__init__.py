@@ -33,6 +33,15 @@ from .ifim import (
     resolve_workers,
     solve_ifim,
 )
+from .pathplan import (
+    BarrierMap,
+    PathPolyline,
+    barrier_speed,
+    gradient_descent_path,
+    plan_path,
+    synthetic_barrier_map,
+    synthetic_endpoints,
+)
 from .result import RunStats, SolverResult
 
 __version__ = "0.1.0"
@@ -42,5 +51,6 @@ __all__ = [
     "PARALLEL_METHODS", "RemedySet", "RunStats", "SolverResult", "build_remedy_set", "clear_workspaces",
     "export_field_npy", "field_digest", "field_max_diff", "field_sha256", "import_field_npy", "ifim_remedy_step", "ifim_update_step", "new_grid", "new_grid_3d",
     "reset_field", "resolve_workers", "run_method", "seed_linear", "seed_point", "solve_fim", "solve_ifim", "solve_fixpoint",
-    "max_residual",
+    "max_residual", "BarrierMap", "PathPolyline", "barrier_speed", "gradient_descent_path", "plan_path",
+    "synthetic_barrier_map", "synthetic_endpoints",
 ]

@@ -113,6 +113,7 @@ struct Ctl {
     unsigned long long nz_words;    // remedy diagnostics: non-empty member words / 4-cell sectors
     unsigned long long nz_sectors;
     unsigned stale;                 // remedy: a hand-built set has members outside its work list (St)
+    unsigned engine;                // remedy: engine chosen on the device (1 member list, 3 brick)
     unsigned wcount;                // multi-rank: world-barrier arrivals (rank 0's copy is used)
     unsigned wgen;                  // multi-rank: this rank's world-barrier generation
     unsigned fc[3];                 // FIM: check-list length per rotating slot
@@ -207,6 +208,7 @@ struct KP {
     uint32_t *bmask;             // [3 slots][nbricks]: which records a brick reads next round
     uint32_t *blist0, *blist1;   // [nbricks]: active bricks of a round, by parity
     unsigned *bcnt;              // [3 slots] list lengths, [3 slots] grab counters (128-byte lines)
+    unsigned *bsel;              // engine selection: [0] skip word of the list kernel, [32] of the brick kernel
     // multi-rank (peer slabs): this rank owns planes [zg0, zg0 + nz) of the global grid
     int32_t mr, q, R, pad2;
     uint32_t gb0, gnb;     // this rank's CTAs: blockIdx.x in [gb0, gb0 + gnb)
@@ -2436,7 +2438,7 @@ int make_layout(const eik_geom *g, Layout &L)
         L.off_bmask = o; o += al(3 * nb * 4);
         L.off_blist0 = o; o += al(nb * 4);
         L.off_blist1 = o; o += al(nb * 4);
-        L.off_bcnt = o; o += al(6 * 128);
+        L.off_bcnt = o; o += al(8 * 128);
     }
     // member-list traversal (word_at): 3D groups of 4x4 rows, 2D groups of 16 rows, per x-word
     if (g->ndim == 3) {
@@ -2519,6 +2521,7 @@ KP make_kp(const eik_geom *g, const Layout &L, void *ws, real_t *phi, const real
     p.blist0 = (uint32_t *)(b + L.off_blist0);
     p.blist1 = (uint32_t *)(b + L.off_blist1);
     p.bcnt = (unsigned *)(b + L.off_bcnt);
+    p.bsel = p.bcnt + 6 * 32;
     return p;
 }
 
@@ -2606,6 +2609,18 @@ int encode_3d(CUtensorMap *tm, CUtensorMapDataType dt, size_t esz, const void *b
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail(EIK_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
     return EIK_OK;
+}
+
+// |R_0| share of the grid (percent) from which the device picks the brick engine (auto mode).
+// Measured (docs/PERF_LOG.md): cfg4 512^3 (|R_0| 4.9 %) member list 268 vs brick 336 ms;
+// cfg5 512^3 (53 %) 322 vs 307 ms, cfg5 1024^3 4.60 vs 4.06 s; cfg3 256^3 4.3 vs 4.8 ms.
+#ifndef BRK_DENSE_PCT
+#define BRK_DENSE_PCT 20
+#endif
+int brick_dense_pct()
+{
+    if (const char *e = getenv("EIK_BRICK_DENSE_PCT")) return atoi(e);
+    return BRK_DENSE_PCT;
 }
 
 // The brick engine needs TMA-legal strides (16-byte multiples), a box no larger than the grid
@@ -2715,7 +2730,7 @@ struct Engine {
         if (rc) return rc;
         CK(cudaMemsetAsync(p.bmask, 0, (size_t)3 * p.nbricks * 4, st));
         CK(cudaMemsetAsync(p.bcnt, 0, 6 * 128, st));
-        k_brick_prep<<<stream_grid((int64_t)p.nbricks), 256, 0, st>>>(p);
+        k_brick_prep<<<stream_grid((int64_t)p.nbricks), 256, 0, st>>>(p, skip);
         CK(cudaGetLastError());
         auto kern = k_remedy_b<SOL>;
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)brk::SMEM));
@@ -2736,9 +2751,22 @@ struct Engine {
     {
         const char *mode = getenv("EIK_REMEDY");
         if constexpr (DIM == 3 && SOL == SOL_U3) {
-            if (!need_tile && brick_eligible(p) && (mode ? strcmp(mode, "brick") == 0 : REMEDY_BRICK_DEFAULT)) {
-                g_remedy_engine = 3;
-                return remedy_brick(p, skip, st);
+            if (!need_tile && brick_eligible(p)) {
+                if (mode && strcmp(mode, "brick") == 0) {
+                    g_remedy_engine = 3;
+                    return remedy_brick(p, skip, st);
+                }
+                if (!mode || strcmp(mode, "auto") == 0) {
+                    // chosen on the device from |R_0| (no host sync): the brick pipeline for dense
+                    // sets, the member list for sparse ones; the other kernel exits at once
+                    k_choose_remedy<<<1, 1, 0, st>>>(p.ctl, skip, p.bsel, (unsigned long long)p.ncells,
+                                                     (unsigned)brick_dense_pct());
+                    CK(cudaGetLastError());
+                    int rc = remedy(p, p.bsel, st);
+                    if (!rc) rc = remedy_brick(p, p.bsel + 32, st);
+                    g_remedy_engine = 4;  // resolved from Ctl::engine after the solve's sync
+                    return rc;
+                }
             }
         }
         const bool tile = need_tile || (mode ? strcmp(mode, "tile") == 0 : REMEDY_TILE_DEFAULT);
@@ -3020,6 +3048,7 @@ int EIK_FN(eik_remedy_step)(const eik_geom *g, real_t *phi, const real_t *speed,
     CK(cudaMemcpyAsync(&c, ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if ((rc = check_hang(c, "remedy step"))) return rc;
+    if (g_remedy_engine == 4) g_remedy_engine = c.engine ? (int)c.engine : 1;
     out->rem_iterations = out->iterations = (int64_t)c.iters;
     out->rem_calls = out->solver_calls = (int64_t)c.sum;
     out->peak_remedy = (int64_t)c.peak;
@@ -3082,6 +3111,7 @@ int EIK_FN(eik_ifim_solve)(const eik_geom *g, real_t *phi, const real_t *speed, 
     CK(cudaMemcpyAsync(&c[1], cr, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if ((rc = check_hang(c[0], "update step")) || (rc = check_hang(c[1], "remedy step"))) return rc;
+    if (g_remedy_engine == 4) g_remedy_engine = c[1].engine ? (int)c[1].engine : 1;
     if (c[0].err == EIK_ECAP) {
         if ((rc = expose_latest(L, c[0], phi, p.P1, st))) return rc;
         return fail(EIK_ECAP, "active list did not drain within %lld iterations", (long long)L.cap_upd);

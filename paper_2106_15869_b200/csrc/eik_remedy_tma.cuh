@@ -143,8 +143,9 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // Round 0 set-up: R_0 rows (the build's row-major bitmap) into record buffer 1, fixed rows
 // brick-major (rows outside the grid: all fixed), list 0 = the bricks holding R_0 members.
 // One warp per brick; lane l handles rows l and l + 32 (row j = plane j / 8, y = j % 8).
-__global__ void __launch_bounds__(256) k_brick_prep(KP p)
+__global__ void __launch_bounds__(256) k_brick_prep(KP p, const unsigned *skip)
 {
+    if (skip && *skip) return;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = lane_id();
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
     for (uint32_t b = warp; b < p.nbricks; b += nwarps) {
@@ -169,6 +170,17 @@ __global__ void __launch_bounds__(256) k_brick_prep(KP p)
             p.blist0[atomicAdd(brk::len_slot(p, 0), 1u)] = b;
         }
     }
+}
+
+// Auto mode: the brick pipeline for dense remedy sets (|R_0| >= pct % of the cells), the member
+// list otherwise.  Writes each kernel's skip word (an update-step error skips both).
+__global__ void k_choose_remedy(Ctl *ctl, const unsigned *skip, unsigned *sel, unsigned long long ncells, unsigned pct)
+{
+    const bool err = skip && *skip;
+    const bool dense = ctl->flagged * 100ull >= (unsigned long long)pct * ncells;
+    sel[0] = err || dense;
+    sel[32] = err || !dense;
+    ctl->engine = dense ? 3u : 1u;
 }
 
 template <int SOL>
