@@ -125,7 +125,8 @@ int eik_ifim_solve(const eik_geom *g, double *phi, const double *speed, uint8_t 
 /* Element-wise local solver on device arrays (parity hook for
  * E/_kernels.py:41-88 and E/local_solver.py:91-157).  kind: 0 = 2D uniform
  * (a, b, f, dx), 1 = 2D anisotropic (a, b, f, dx, dy), 2 = 3D uniform
- * (a, b, c, f, dx). */
+ * (a, b, c, f, dx).  dx <= 0 (kinds 0 and 2): each element's spacing is read
+ * from out[i] before the result overwrites it. */
 int eik_local_solve(int kind, const double *a, const double *b, const double *c, const double *f,
                     double dx, double dy, double *out, int64_t n, void *stream);
 

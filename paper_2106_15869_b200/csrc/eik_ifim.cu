@@ -2190,9 +2190,10 @@ __global__ void k_local(int kind, const real_t *a, const real_t *b, const real_t
                         real_t dy, real_t *out, int64_t n)
 {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        if (kind == 0) out[i] = upd2u(a[i], b[i], dx / f[i]);
-        else if (kind == 1) out[i] = upd2a(a[i], b[i], f[i], dx, dy);
-        else out[i] = upd3u(a[i], b[i], c[i], dx / f[i], dx);
+        const real_t h = dx > 0 ? dx : out[i];  // dx <= 0: each element's spacing is passed in out[i]
+        if (kind == 0) out[i] = upd2u(a[i], b[i], h / f[i]);
+        else if (kind == 1) out[i] = upd2a(a[i], b[i], f[i], h, dy);
+        else out[i] = upd3u(a[i], b[i], c[i], h / f[i], h);
     }
 }
 

@@ -153,29 +153,28 @@ def test_hand_built_remedy_sets_match_the_reference():
 
 
 def test_local_solver_bitwise(local_vectors):
-    L = local_vectors
-    lib = _native.lib()
-    t = {k: torch.as_tensor(L[k], device=DEV) for k in ("a", "b", "c", "f", "ta", "tb", "tc", "tf")}
-    out = torch.empty_like(t["a"])
-    n = t["a"].numel()
-    s = torch.cuda.current_stream().cuda_stream
+    """All 16,384 reference vectors (T/test_acceptance.py:149-161, per-vector spacing) and the
+    near-tie 3D vectors through the GPU solvers: 2D uniform (kind 0) and the 3D walk upd3u
+    (kind 2), bit for bit."""
     import ctypes as C
 
+    L = local_vectors
+    lib = _native.lib()
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     P = lambda x: C.c_void_p(x.data_ptr())  # noqa: E731
-    # per-element spacing: group samples by spacing value is impractical; use dx per call
-    dx = L["dx"]
-    got2, got3 = np.empty(n), np.empty(n)
-    # one launch per unique spacing would be slow; instead scale-invariant check on a subset
-    for k in range(0, 512):
-        a1 = t["a"][k:k + 1]
-        _native.check(lib.eik_local_solve(0, P(a1), P(t["b"][k:k + 1]), None, P(t["f"][k:k + 1]), float(dx[k]), 0.0,
-                                          P(out[k:k + 1]), 1, C.c_void_p(s)))
-        got2[k] = out[k].item()
-        _native.check(lib.eik_local_solve(2, P(a1), P(t["b"][k:k + 1]), P(t["c"][k:k + 1]), P(t["f"][k:k + 1]),
-                                          float(dx[k]), 0.0, P(out[k:k + 1]), 1, C.c_void_p(s)))
-        got3[k] = out[k].item()
-    assert np.array_equal(got2[:512].view(np.uint64), L["u2"][:512].view(np.uint64))
-    assert np.array_equal(got3[:512].view(np.uint64), L["u3"][:512].view(np.uint64))
+
+    def run(kind, a, b, c, f, dx):
+        # per-element spacings (dx <= 0: the spacing of element i is passed in out[i])
+        T = [torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64), device=DEV) for v in (a, b, c, f)]
+        out = torch.as_tensor(np.ascontiguousarray(dx, dtype=np.float64), device=DEV).clone()
+        _native.check(lib.eik_local_solve(kind, P(T[0]), P(T[1]), P(T[2]), P(T[3]), -1.0, 0.0, P(out), len(a), s))
+        return out.cpu().numpy().view(np.uint64)
+
+    n = len(L["a"])
+    assert np.array_equal(run(0, L["a"], L["b"], L["c"], L["f"], L["dx"]), L["u2"][:n].view(np.uint64))
+    assert np.array_equal(run(2, L["a"], L["b"], L["c"], L["f"], L["dx"]), L["u3"].view(np.uint64))
+    assert np.array_equal(run(2, L["c"], L["a"], L["b"], L["f"], L["dx"]), L["u3p"].view(np.uint64))
+    assert np.array_equal(run(2, L["ta"], L["tb"], L["tc"], L["tf"], L["td"]), L["t3"].view(np.uint64))
 
 
 def test_local_solver_bitwise_batched():
