@@ -209,7 +209,8 @@ const char *eik_last_error(void);
 const char *eik_version(void);
 /* Which engine ran the calling thread's last remedy step: 0 none, 1 member list (k_remedy),
  * 2 tile (k_remedy_t), 3 TMA brick pipeline (k_remedy_b).  Selection: EIK_REMEDY=list|tile|brick,
- * else the default (3D single device: brick when eligible). */
+ * else auto (3D single device, brick-eligible geometry: the device picks the brick engine when
+ * |R_0| >= 20 % of the cells (EIK_BRICK_DENSE_PCT), the member list otherwise). */
 int eik_last_remedy_engine(void);
 
 /* ---- float32 perf mode (libeik_ifim_f32.so) ----
