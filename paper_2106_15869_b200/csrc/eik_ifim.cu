@@ -851,6 +851,9 @@ __global__ void k_init_active(KP p, const int64_t *seeds, int64_t nseeds)
 #ifndef UPD_MU
 #define UPD_MU 1  // active cells per thread per pass (2 measured slower: 47 vs 37 ms at 512^3)
 #endif
+#ifndef UPD_PREF
+#define UPD_PREF 1  // first-pass list entry loaded with the list length after each barrier
+#endif
 // Sum of a worklist-length slot over all ranks (multi-rank) or this rank.
 template <bool MR>
 __device__ __forceinline__ unsigned long long ranks_len(const KP &p, int slot)
@@ -891,6 +894,11 @@ __device__ __forceinline__ void update_body(const KP &p)
     }
     const uint32_t nx = (uint32_t)p.nx, ny = (uint32_t)p.ny, nz = (uint32_t)p.nz;
     unsigned nnext = ~0u;  // next iteration's list length when already read
+    // UPD_PREF: this thread's first list entry of the next iteration, loaded right after the barrier
+    // together with the list length (the two L2 round trips overlap); entries past the length are
+    // stale and masked by `live`
+    uint32_t pre = 0;
+    bool have_pre = false;
     for (int64_t it = p.it0; it < p.it0 + p.max_it; ++it) {
         const int par = (int)(it & 1);
         const real_t *__restrict__ Pc = par ? p.P1 : p.P0;
@@ -911,7 +919,8 @@ __device__ __forceinline__ void update_body(const KP &p)
                 const unsigned i = base + u * BLOCK + threadIdx.x;
                 live[u] = i < n;
                 emit[u] = 0;
-                c[u] = live[u] ? __ldcg(Lc + i) : 0u;
+                if (UPD_PREF && u == 0 && have_pre && base == gb * (BLOCK * UPD_MU)) c[u] = live[u] ? pre : 0u;
+                else c[u] = live[u] ? __ldcg(Lc + i) : 0u;
                 carry[u] = (c[u] & CARRY) != 0;  // non-converged in the previous iteration
                 c[u] &= ~CARRY;
                 r[u] = fdiv(c[u], p.fnx);
@@ -1019,6 +1028,11 @@ __device__ __forceinline__ void update_body(const KP &p)
             ctl->len[(it + 2) % 3] = 0;
         }
         if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
+        if (UPD_PREF && !MR) {
+            const unsigned i0 = gb * (BLOCK * UPD_MU) + threadIdx.x;
+            pre = i0 < (unsigned)p.ncells ? __ldcg(Ln + i0) : 0u;
+            have_pre = true;
+        }
         const unsigned long long m = ranks_len<MR>(p, (int)((it + 1) % 3));
         nnext = MR ? ~0u : (unsigned)m;
 #ifdef EIK_DIAG
