@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py tests/test_gpu_brick.py tests/test_gpu_fuzz.py -x -q -p no:cacheprovider > gpurun_out/r15_tests.log 2>&1; echo "tests rc=$?"; tail -2 gpurun_out/r15_tests.log
+timeout 900 python tools/ab.py --n 512 --kind checker libeik_head.so libeik_ifim.so libeik_head.so:EIK_REMEDY=brick libeik_ifim.so:EIK_REMEDY=brick > gpurun_out/r15_ab_cfg4.log 2>&1; cat gpurun_out/r15_ab_cfg4.log
+timeout 900 python tools/ab.py --n 512 --kind cfg5 libeik_head.so libeik_ifim.so libeik_head.so:EIK_REMEDY=list libeik_ifim.so:EIK_REMEDY=list > gpurun_out/r15_ab_cfg5.log 2>&1; cat gpurun_out/r15_ab_cfg5.log
