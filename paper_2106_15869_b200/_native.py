@@ -201,8 +201,7 @@ REMEDY_ENGINES = {0: "none", 1: "list", 2: "tile", 3: "brick"}
 
 def last_remedy_engine(dtype: int = EIK_F64) -> str:
     """Engine of this thread's last remedy step (list / tile / brick, eik_last_remedy_engine)."""
-    L = lib(dtype)
-    return REMEDY_ENGINES[int((L.eik_last_remedy_engine_f32 if dtype == EIK_F32 else L.eik_last_remedy_engine)())]
+    return REMEDY_ENGINES[int(lib(dtype).eik_last_remedy_engine())]  # the float32 library appends _f32 itself
 
 
 def check(rc: int, dtype: int | None = None) -> None:

@@ -110,3 +110,22 @@ def test_fastdiv_exact_below_2_31(d):
     for n in ns.tolist():
         if n < 2 ** 31:
             assert f(n) == n // d, (n, d)
+
+
+def test_last_remedy_engine_both_dtypes():
+    """eik_last_remedy_engine(_f32) is callable through the package for both libraries (no GPU
+    needed: it reads the calling thread's last choice; a fresh thread has none)."""
+    import threading
+
+    from paper_2106_15869_b200 import _native
+
+    out = {}
+
+    def probe():
+        out["f64"] = _native.last_remedy_engine(_native.EIK_F64)
+        out["f32"] = _native.last_remedy_engine(_native.EIK_F32)
+
+    t = threading.Thread(target=probe)
+    t.start()
+    t.join()
+    assert out == {"f64": "none", "f32": "none"}

@@ -197,3 +197,29 @@ def test_bench_json_contract_small():
         assert k in d["roofline"], k
     assert d["e2e"]["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] > 0 and d["gpu_launches"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
+
+
+@pytest.mark.parametrize("extra,dtype,engine", [(["--dtype", "f32"], "f32", None),
+                                                (["--config", "cfg5", "--size", "64"], "f64", "brick"),
+                                                (["--config", "cfg1", "--size", "64"], "f64", None)])
+def test_bench_variants_small(extra, dtype, engine):
+    """bench.py's other modes end to end on small grids: the float32 perf mode, the brick remedy
+    engine (forced) and a 2D config; each prints a valid line naming the engine that ran."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ)
+    if engine:
+        env["EIK_REMEDY"] = engine
+    args = [sys.executable, os.path.join(root, "bench.py"), "--steps", "1", "--warmup", "3", "--no-cpu", "--no-e2e"]
+    if "--size" not in extra:
+        args += ["--size", "64"]
+    out = subprocess.run(args + extra, capture_output=True, text=True, timeout=600, env=env)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    assert d["value"] > 0 and d["dtype"] == dtype
+    if engine:
+        assert d["config"]["remedy_engine"] == engine, d["config"]
