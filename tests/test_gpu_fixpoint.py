@@ -201,10 +201,15 @@ def test_bench_json_contract_small():
 
 @pytest.mark.parametrize("extra,dtype,engine", [(["--dtype", "f32"], "f32", None),
                                                 (["--config", "cfg5", "--size", "64"], "f64", "brick"),
-                                                (["--config", "cfg1", "--size", "64"], "f64", None)])
+                                                (["--config", "cfg1", "--size", "64"], "f64", None),
+                                                (["--config", "cfg2", "--size", "128"], "f64", None),
+                                                (["--config", "cfg3", "--size", "64"], "f64", None),
+                                                (["--method", "fim"], "f64", None),
+                                                (["--slabs"], "f64", None)])
 def test_bench_variants_small(extra, dtype, engine):
     """bench.py's other modes end to end on small grids: the float32 perf mode, the brick remedy
-    engine (forced) and a 2D config; each prints a valid line naming the engine that ran."""
+    engine (forced), the 2D configs, cfg3, the FIM baseline and the one-GPU slab protocol; each
+    prints a valid line (and names the remedy engine that ran when one is forced)."""
     import json
     import os
     import subprocess
