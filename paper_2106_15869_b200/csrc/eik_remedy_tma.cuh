@@ -340,10 +340,16 @@ __global__ void __launch_bounds__(brk::THREADS, BRK_CTAS)
                 const bool xy_edge = x0 == 0 || x0 + BX >= nx || y0 == 0 || y0 + BY >= ny;
                 if (xy_edge && z < nz) {
                     real_t *pl = box + (warp + 1u) * (HX * HY);
-                    for (uint32_t i = lane; i < (uint32_t)(HX * HY); i += 32) {
-                        const uint32_t iy = i / HX, ix = i - iy * HX;
-                        const int gx = (int)(x0 + ix) - XP, gy = (int)(y0 + iy) - 1;
-                        if (gx < 0 || gx >= (int)nx || gy < 0 || gy >= (int)ny) pl[i] = INFINITY;
+                    // box columns [0, xl) and [xh, HX), rows [0, yl) and [yh, HY) lie outside the grid
+                    const uint32_t xl = x0 == 0 ? (uint32_t)XP : 0u, xh = min((uint32_t)HX, XP + nx - x0);
+                    const uint32_t yl = y0 == 0 ? 1u : 0u, yh = min((uint32_t)HY, 1u + ny - y0);
+                    for (uint32_t iy = 0; iy < (uint32_t)HY; ++iy)
+                        if (iy < yl || iy >= yh)
+                            for (uint32_t ix = lane; ix < (uint32_t)HX; ix += 32) pl[iy * HX + ix] = INFINITY;
+                    const uint32_t nc = xl + (HX - xh);  // out-of-grid columns per row
+                    for (uint32_t k = lane; k < nc * (yh - yl); k += 32) {
+                        const uint32_t r = k / nc, cc = k - r * nc;
+                        pl[(yl + r) * HX + (cc < xl ? cc : xh + (cc - xl))] = INFINITY;
                     }
                     __syncwarp();
                 }
