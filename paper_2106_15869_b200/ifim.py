@@ -133,13 +133,15 @@ class _HostResult:
 
     Large fields: the copy is allocated on a helper thread while the device
     solves (the engine call releases the GIL).  A pinned caller array gets a
-    pinned copy (torch's caching host allocator reuses freed ones) filled by a
-    second device-to-host DMA, so no host memcpy is on the critical path.  A
+    pinned copy (torch's caching host allocator reuses freed ones); the field is
+    downloaded once, in chunks, and each chunk is copied into the result on the
+    host while the later chunks are still in flight.  A
     pageable caller array gets a first-touched pageable copy; the field is
     downloaded once into the caller's array and the copy is a host memcpy of it.
     """
 
     MIN_CELLS = 1 << 22
+    CHUNK_BYTES = 1 << 27  # D2H chunk of the pinned path
 
     def __init__(self, dg):
         self.dg, self.buf, self.thread = dg, None, None
@@ -170,9 +172,22 @@ class _HostResult:
         host = torch.from_numpy(gphi) if isinstance(gphi, np.ndarray) else gphi
         dev = dg.phi.reshape(host.shape)
         if self.pinned:
-            host.copy_(dev, non_blocking=True)
-            buf.copy_(dev, non_blocking=True)
-            torch.cuda.current_stream(dg.device).synchronize()
+            # one DMA into the caller's array, chunk by chunk; each landed chunk is copied into the
+            # result on the host (torch's threaded copy) while the next chunks are in flight
+            st = torch.cuda.current_stream(dg.device)
+            hf, df, bf = host.reshape(-1), dev.reshape(-1), buf.reshape(-1)
+            n = hf.numel()
+            step = max(1, self.CHUNK_BYTES // hf.element_size())
+            landed = []
+            for a in range(0, n, step):
+                b = min(n, a + step)
+                hf[a:b].copy_(df[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(st)
+                landed.append((a, b, ev))
+            for a, b, ev in landed:
+                ev.synchronize()
+                bf[a:b].copy_(hf[a:b])
         else:
             dg.commit(phi=True)
             buf.copy_(host)

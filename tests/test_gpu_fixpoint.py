@@ -228,3 +228,25 @@ def test_bench_variants_small(extra, dtype, engine):
     assert d["value"] > 0 and d["dtype"] == dtype
     if engine:
         assert d["config"]["remedy_engine"] == engine, d["config"]
+
+
+def test_pinned_host_grid_result_copy():
+    """A pinned CPU-tensor grid (the chunked download + overlapped host result copy of
+    ifim._HostResult): grid.phi holds the solution in place, SolverResult.phi is a separate copy
+    with the same bytes, both equal to the solve of the same problem on CUDA tensors."""
+    n = 164  # > 2^22 cells: the large-field path
+    k = np.arange(n) // 8
+    F = np.where((k[:, None, None] + k[None, :, None] + k[None, None, :]) % 2 == 0, 1.0, 0.05)
+    pin = lambda a: torch.as_tensor(a).pin_memory()  # noqa: E731
+    g = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), pin(np.full((n, n, n), np.inf)), pin(F),
+                   pin(np.zeros((n, n, n), np.uint8)))
+    res = eik.solve_ifim(g, eik.seed_point(g, eik.CellIndex3D(3, n // 2, n - 5), 0.0))
+    dev = torch.device("cuda:0")
+    g2 = eik.Grid3D(n, n, n, 1.0, (0.0, 0.0, 0.0), torch.full((n, n, n), float("inf"), dtype=torch.float64, device=dev),
+                    torch.as_tensor(F, device=dev), torch.zeros((n, n, n), dtype=torch.uint8, device=dev))
+    ref = eik.solve_ifim(g2, eik.seed_point(g2, eik.CellIndex3D(3, n // 2, n - 5), 0.0))
+    assert res.phi.data_ptr() != g.phi.data_ptr()
+    want = ref.phi.cpu().numpy().view(np.uint64)
+    assert np.array_equal(g.phi.numpy().view(np.uint64), want)
+    assert np.array_equal(res.phi.numpy().view(np.uint64), want)
+    assert res.stats.solver_calls == ref.stats.solver_calls
