@@ -605,6 +605,41 @@ def run_e2e_peer(torch, dev, w, world, rank, calls, args):
 FULLSIZE = os.path.join(ROOT, "tests", "golden", "fullsize.json")
 
 
+FULLSIZE_GPU = os.path.join(ROOT, "tests", "golden", "fullsize_gpu.json")
+
+
+def parity_vs_crosscheck(w, r, world, s):
+    """Sizes without an oracle run (cfg5 at 1024^3): the phi digest (chunked device SHA-256) and
+    every RunStats integer against tests/golden/fullsize_gpu.json, the digest three independent
+    device implementations of the remedy agreed on (tools/make_gpu_crosscheck.py)."""
+    import hashlib
+
+    try:
+        with open(FULLSIZE_GPU) as fh:
+            rec = json.load(fh).get(f"{w.name}@{w.n}")
+    except OSError:
+        rec = None
+    if rec is None or world > 1:
+        return "unpinned", f"no full-size digest for {w.name}@{w.n}"
+    from paper_2106_15869_b200.harness import field_digest
+
+    if field_digest(w.F) != rec["speed_field_digest"]:
+        return "unpinned", "speed field differs from the digested one"
+    ph = s.phases
+    got = {"iterations": s.iterations, "solver_calls": s.solver_calls, "peak_active": s.peak_active,
+           "peak_remedy": s.peak_remedy, "phi_writes": s.phi_writes, "upd_iterations": ph["update"]["iterations"],
+           "upd_calls": ph["update"]["solver_calls"], "frozen": ph["update"]["converged"],
+           "build_calls": ph["build"]["solver_calls"], "remedy_size": ph["build"]["remedy_size"],
+           "rem_iterations": ph["remedy"]["iterations"], "rem_calls": ph["remedy"]["solver_calls"],
+           "active_history_sha256": hashlib.sha256(np.asarray(s.active_history, dtype=np.int64).tobytes()).hexdigest(),
+           "phi_field_digest": field_digest(r.phi)}
+    bad = [k for k in got if got[k] != rec[k]]
+    if bad:
+        return "mismatch", "; ".join(f"{k}: {got[k]} != {rec[k]}" for k in bad)
+    return "crosscheck-match", (f"phi digest + {len(got) - 1} RunStats fields equal the GPU cross-check digest "
+                                f"({w.name}@{w.n}: {' == '.join(rec['agreed_by'])}; no oracle run at this size)")
+
+
 def parity_vs_oracle(torch, w, r, world, rank, dtype):
     """After the timed steps: the last solve's phi sha256 and every RunStats integer against the
     full-size oracle digests (tests/golden/fullsize.json, made by tests/golden/make_fullsize.py
@@ -623,7 +658,7 @@ def parity_vs_oracle(torch, w, r, world, rank, dtype):
     except OSError:
         rec = None
     if rec is None:
-        return "unpinned", f"no full-size oracle digest for {w.name}@{w.n}"
+        return parity_vs_crosscheck(w, r, world, s)
     h = hashlib.sha256()
     if world > 1:
         import torch.distributed as dist

@@ -92,3 +92,31 @@ def test_fullsize_composed_equals_oracle_digests(key):
     assert int(torch.isfinite(res.phi).sum()) == rec["phi_finite"]
     del g, res
     torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_cfg5_1024_gpu_crosscheck_digest():
+    """cfg5 at its BASELINE size (1024^3), where no oracle run exists: the composed solve (auto
+    remedy engine) reproduces the digest that the member-list kernel, the TMA brick pipeline and
+    the emulated two-rank peer-slab kernels agreed on (tests/golden/fullsize_gpu.json, made by
+    tools/make_gpu_crosscheck.py): phi (chunked device SHA-256) and every RunStats integer."""
+    from paper_2106_15869_b200.harness import field_digest
+
+    with open(os.path.join(HERE, "golden", "fullsize_gpu.json")) as fh:
+        rec = json.load(fh)["cfg5@1024"]
+    w = bench.make_workload(torch, DEV, "cfg5", 1024)
+    assert field_digest(w.F) == rec["speed_field_digest"]
+    g = w.grid(eik, torch.full(w.shape, float("inf"), dtype=torch.float64, device=DEV), w.F,
+               torch.zeros(w.shape, dtype=torch.uint8, device=DEV))
+    res = eik.solve_ifim(g, w.bc(eik))
+    s, ph = res.stats, res.stats.phases
+    got = {"iterations": s.iterations, "solver_calls": s.solver_calls, "peak_active": s.peak_active,
+           "peak_remedy": s.peak_remedy, "phi_writes": s.phi_writes, "upd_iterations": ph["update"]["iterations"],
+           "rem_iterations": ph["remedy"]["iterations"], "remedy_size": ph["build"]["remedy_size"],
+           "frozen": ph["update"]["converged"],
+           "active_history_sha256": hashlib.sha256(np.asarray(s.active_history, dtype=np.int64).tobytes()).hexdigest(),
+           "phi_field_digest": field_digest(res.phi)}
+    assert got == {k: rec[k] for k in got}
+    del g, res
+    eik.clear_workspaces()
+    torch.cuda.empty_cache()
