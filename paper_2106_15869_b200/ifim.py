@@ -188,7 +188,11 @@ class _HostResult:
         buf = self.buf
         host = torch.from_numpy(gphi) if isinstance(gphi, np.ndarray) else gphi
         dev = dg.phi.reshape(host.shape)
-        if self.pinned:
+        if self.pinned and not host.is_contiguous():
+            host.copy_(dev, non_blocking=True)
+            buf.copy_(dev, non_blocking=True)
+            torch.cuda.current_stream(dg.device).synchronize()
+        elif self.pinned:
             # one DMA into the caller's array, chunk by chunk; the result gets RESULT_DMA_FRAC of the
             # chunks by a second DMA and the others by host copies (torch's threaded copy) of the
             # landed chunks while the next chunks are in flight

@@ -173,3 +173,18 @@ def test_field_npy_round_trip_3d(tmp_path):
                    torch.zeros((4, 5, 7), dtype=torch.uint8))
     eik.export_field_npy(t, p)
     assert np.array_equal(np.load(p).view(np.uint64), g.phi.view(np.uint64))
+
+
+def test_result_split_accounts_every_byte(monkeypatch):
+    """bench's e2e byte counts come from ifim._HostResult.result_split, which must mirror commit():
+    every chunk of the result goes either by a second DMA or by a host copy."""
+    from paper_2106_15869_b200.ifim import _HostResult
+
+    n = 512 ** 3 * 8
+    for frac, want_dma in (("0", 0), ("1", n), ("0.25", n // 4), ("0.5", n // 2)):
+        monkeypatch.setenv("EIK_RESULT_DMA_FRAC", frac)
+        dma, host = _HostResult.result_split(n, 8)
+        assert dma + host == n and dma == want_dma, (frac, dma, host)
+    monkeypatch.delenv("EIK_RESULT_DMA_FRAC")
+    dma, host = _HostResult.result_split(1000 * 8, 8)  # one short chunk
+    assert dma + host == 8000
