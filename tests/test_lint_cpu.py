@@ -17,7 +17,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 FILES = ["bench.py", "__graft_entry__.py"] + sorted(
     os.path.join("paper_2106_15869_b200", f) for f in os.listdir(os.path.join(ROOT, "paper_2106_15869_b200"))
     if f.endswith(".py")) + sorted(
-    os.path.join("tests", f) for f in os.listdir(os.path.join(ROOT, "tests")) if f.endswith(".py"))
+    os.path.join("tests", f) for f in os.listdir(os.path.join(ROOT, "tests")) if f.endswith(".py")) + sorted(
+    os.path.join(d, f) for d in ("tools", "oracle", os.path.join("tests", "golden"))
+    for f in os.listdir(os.path.join(ROOT, d)) if f.endswith(".py"))
 
 
 def _undefined(path):
