@@ -1,4 +1,4 @@
-"""Turn ncu outputs brought back in gpurun_out/ into committed summaries under profiles/.
+"""(Round 1; superseded by tools/summarize_r2.py, whose ncu_summary.json schema bench.py reads.) Turn ncu outputs brought back in gpurun_out/ into committed summaries under profiles/.
 
     python tools/summarize_profiles.py --launches gpurun_out/launches_rX.csv \
         --full gpurun_out/prof_rX.ncu-rep --tag rX --workload "<bench workload string>"
