@@ -222,9 +222,6 @@ struct KP {
 #ifndef REMEDY_TILE_DEFAULT
 #define REMEDY_TILE_DEFAULT 0  // single-device remedy: 1 = tile engine, 0 = member-list kernel
 #endif
-#ifndef REMEDY_BRICK_DEFAULT
-#define REMEDY_BRICK_DEFAULT 0  // single-device 3D remedy: 1 = brick engine (TMA), 0 = as below
-#endif
 #ifndef RT_SHARDS
 #define RT_SHARDS 32
 #endif
@@ -1286,106 +1283,6 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
     }
 }
 
-#ifndef REM_ASYNC
-#define REM_ASYNC 0  // 1: phase A gathers by cp.async into a per-warp double buffer (measured slower, PERF_LOG)
-#endif
-constexpr uint32_t NO_ENTRY = 0xffffffffu;
-
-// Asynchronous 4/8-byte global -> shared copy (L1-allocating), commit / wait on this thread's groups.
-__device__ __forceinline__ void cp_async(real_t *s, const real_t *g)
-{
-    const unsigned a = (unsigned)__cvta_generic_to_shared(s);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(a), "l"(g), "n"((int)sizeof(real_t)) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
-
-// Issue the stencil copies of one member (list entry e, NO_ENTRY for none) into its lane's slots
-// sl[k * 32], k = c, w, e, s, n, d, u, coefficient; out-of-grid neighbours are +inf
-// (E/_kernels.py:21-38).  Returns row * 32W + x (its D word and bit), or NO_ENTRY.
-template <int DIM, int SOL>
-__device__ __forceinline__ uint32_t gather_async(const KP &p, const real_t *__restrict__ Pc, uint32_t e, real_t *sl)
-{
-    if (e == NO_ENTRY) return NO_ENTRY;
-    const uint32_t c = e & ~CARRY;
-    const uint32_t row = fdiv(c, p.fnx), x = c - row * p.nx32;
-    uint32_t y = row, z = 0;
-    if (DIM == 3) {
-        z = fdiv(row, p.fny);
-        y = row - z * (uint32_t)p.ny;
-    }
-    cp_async(sl, Pc + c);
-    if (x > 0) cp_async(sl + 32, Pc + (c - 1)); else sl[32] = INFINITY;
-    if (x + 1 < p.nx32) cp_async(sl + 64, Pc + (c + 1)); else sl[64] = INFINITY;
-    if (y > 0) cp_async(sl + 96, Pc + (c - p.nx32)); else sl[96] = INFINITY;
-    if (y + 1 < (uint32_t)p.ny) cp_async(sl + 128, Pc + (c + p.nx32)); else sl[128] = INFINITY;
-    if (DIM == 3) {
-        if (z > 0) cp_async(sl + 160, Pc + (c - p.plane32)); else sl[160] = INFINITY;
-        if (z + 1 < (uint32_t)p.nz) cp_async(sl + 192, Pc + (c + p.plane32)); else sl[192] = INFINITY;
-    }
-    cp_async(sl + 224, (SOL == SOL_A2 ? p.F : p.dd) + c);
-    return row * (p.W * 32u) + x;
-}
-
-// Phase A of one remedy round on a CTA's list segment [sbeg, mend): each warp relaxes 32
-// members per step while the copies of its next 32 are in flight.  Returns the decreases.
-template <int DIM, int SOL>
-__device__ __forceinline__ unsigned long long rem_phaseA_async(const KP &p, const uint32_t *__restrict__ ML,
-                                                               uint32_t sbeg, uint32_t mend,
-                                                               const real_t *__restrict__ Pc, real_t *__restrict__ Pn,
-                                                               uint32_t *Dc, real_t *stg)
-{
-    const unsigned lane = lane_id();
-    const uint32_t ws = WPB * 32;
-    const uint32_t wb = sbeg + (threadIdx.x >> 5) * 32;
-    unsigned long long a_dec = 0;
-    auto entry = [&](uint32_t i) { return i + lane < mend ? __ldcg(ML + i + lane) : NO_ENTRY; };
-    uint32_t ecur = entry(wb);
-    uint32_t pcur = gather_async<DIM, SOL>(p, Pc, ecur, stg + lane);
-    cp_async_commit();
-    uint32_t enext = entry(wb + ws);
-    uint32_t k = 0;
-    for (uint32_t i = wb; i < mend; i += ws, ++k) {
-        real_t *cur = stg + (k & 1) * 256 + lane;
-        const uint32_t pnext = gather_async<DIM, SOL>(p, Pc, enext, stg + ((k + 1) & 1) * 256 + lane);
-        cp_async_commit();
-        const uint32_t enn = entry(i + 2 * ws);
-        cp_async_wait<1>();  // this step's copies have landed
-        bool dec = false;
-        if (ecur != NO_ENTRY) {
-            Sten s;
-            s.c = cur[0]; s.w = cur[32]; s.e = cur[64]; s.s = cur[96]; s.n = cur[128];
-            s.d = DIM == 3 ? cur[160] : INFINITY;
-            s.u = DIM == 3 ? cur[192] : INFINITY;
-            s.k = cur[224];
-            const real_t v = solve<DIM, SOL>(p, s);
-            const uint32_t c = ecur & ~CARRY;
-            dec = v < s.c - tol_at(p.tol, s.c);  // E/ifim.py:203
-            if (dec) Pn[c] = v;
-            else if (ecur & CARRY) Pn[c] = s.c;  // changed last round: carry into the other buffer
-        }
-        // D_r bits: a warp's members of one word are contiguous in the list (segmented OR-scan,
-        // one atomicOr per word)
-        a_dec += __popc(__ballot_sync(FULL, dec));
-        const uint32_t wi = ecur != NO_ENTRY ? pcur >> 5 : 0xffffffffu;
-        uint32_t acc = dec ? (1u << (pcur & 31u)) : 0u;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t ov = __shfl_down_sync(FULL, acc, o);
-            const uint32_t ow = __shfl_down_sync(FULL, wi, o);
-            if (lane + o < 32 && ow == wi) acc |= ov;
-        }
-        const uint32_t pw = __shfl_up_sync(FULL, wi, 1);
-        if (acc && (lane == 0 || pw != wi)) atomicOr(Dc + wi, acc);
-        ecur = enext;
-        pcur = pnext;
-        enext = enn;
-    }
-    cp_async_wait<0>();
-    return a_dec;
-}
-
 #ifndef REM_MINB
 #define REM_MINB 4
 #endif
@@ -1394,7 +1291,6 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
 {
     __shared__ unsigned sscan[WPB + 1];
     __shared__ unsigned long long sred[WPB];
-    __shared__ real_t s_stage[(!MR && REM_ASYNC) ? WPB * 2 * 256 : 1];  // per warp: 2 steps x 8 values x 32 lanes
     if (skip && *skip) return;
     Ctl *ctl = p.ctl;
     const unsigned lane = lane_id();
@@ -1466,9 +1362,6 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
         const uint32_t seg = ((m + gnb - 1) / gnb + 32 * REM_MU - 1) / (32 * REM_MU) * (32 * REM_MU);
         const uint32_t sbeg = gb * seg, mend = min(m, sbeg + seg);
         const uint32_t wbase = sbeg + (threadIdx.x >> 5) * 32 * REM_MU, wstride = WPB * 32 * REM_MU;
-        if (!MR && REM_ASYNC)
-            a_dec = rem_phaseA_async<DIM, SOL>(p, ML, sbeg, mend, Pc, Pn, Dc, s_stage + (threadIdx.x >> 5) * 512);
-        else
         for (uint32_t i0 = wbase; i0 < mend; i0 += wstride) {
             uint32_t ent[REM_MU], rw[REM_MU], x[REM_MU];
             bool live[REM_MU];
