@@ -8,6 +8,9 @@
 //   remedy step  (E/ifim.py:164-218) -> k_remedy   persistent; per round the member list is
 //                                                  rebuilt from the decrease bitmap, then one
 //                                                  thread per member
+//                                     or k_remedy_b (eik_remedy_tma.cuh) TMA brick pipeline for
+//                                                  dense remedy sets, chosen on the device from
+//                                                  |R_0| (k_choose_remedy)
 // plus the fixpoint ground truth (E/oracle.py, k_fixpoint), max_residual
 // (E/harness.py, k_residual), the FIM baseline (E/fim.py, k_fim) and the
 // multi-rank z-slab variants of the update / remedy kernels (peer memory).
