@@ -76,7 +76,10 @@ typedef double real_t;
 namespace {
 
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int BLOCK = 256;
+#ifndef EIK_BLOCK
+#define EIK_BLOCK 256
+#endif
+constexpr int BLOCK = EIK_BLOCK;
 constexpr int WPB = BLOCK / 32;
 constexpr uint8_t ST_SOURCE = 2, ST_BLOCKED = 4;  // E/grid.py:21-26
 enum { SOL_U2 = 0, SOL_A2 = 1, SOL_U3 = 2 };
@@ -525,7 +528,8 @@ __device__ __forceinline__ T warp_sum(T v)
     return v;
 }
 
-// Sum a per-thread value over the block; result valid in thread 0.
+// Sum a per-thread value over the block of NT threads; result valid in thread 0.
+template <int NT = BLOCK>
 __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, unsigned long long *sm)
 {
     v = warp_sum(v);
@@ -535,7 +539,7 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, un
     __syncthreads();
     unsigned long long t = 0;
     if (threadIdx.x == 0)
-        for (int i = 0; i < WPB; ++i) t += sm[i];
+        for (int i = 0; i < NT / 32; ++i) t += sm[i];
     __syncthreads();
     return t;
 }
@@ -684,7 +688,7 @@ constexpr uint32_t CARRY = 0x80000000u;
 
 // Block-wide exclusive scan of a per-thread count plus one global reservation:
 // returns this thread's first slot in the global list whose length is *glen.
-template <bool SYS = false>
+template <bool SYS = false, int NT = BLOCK>
 __device__ __forceinline__ unsigned block_reserve(unsigned v, unsigned *glen, unsigned *sscan)
 {
     const unsigned lane = lane_id(), warp = threadIdx.x >> 5;
@@ -698,15 +702,15 @@ __device__ __forceinline__ unsigned block_reserve(unsigned v, unsigned *glen, un
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned acc = 0;
-        for (int i = 0; i < WPB; ++i) {
+        for (int i = 0; i < (NT / 32); ++i) {
             const unsigned t = sscan[i];
             sscan[i] = acc;
             acc += t;
         }
-        sscan[WPB] = acc ? (SYS ? atomicAdd_system(glen, acc) : atomicAdd(glen, acc)) : 0u;
+        sscan[(NT / 32)] = acc ? (SYS ? atomicAdd_system(glen, acc) : atomicAdd(glen, acc)) : 0u;
     }
     __syncthreads();
-    const unsigned pos = sscan[WPB] + sscan[warp] + inc - v;
+    const unsigned pos = sscan[(NT / 32)] + sscan[warp] + inc - v;
     __syncthreads();
     return pos;
 }
@@ -1209,13 +1213,13 @@ __global__ void k_remedy_export(KP p, uint8_t *member)
 #endif
 
 
-template <int DIM, bool MR>
+template <int DIM, bool MR, int NT>
 __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint32_t *__restrict__ Dp,
                                             uint32_t *Dc, uint32_t *ML, unsigned *lenR, unsigned *sscan, unsigned gb,
                                             unsigned gnb)
 {
     const unsigned lane = lane_id();
-    const uint32_t chunk = BLOCK * REM_PER;
+    const uint32_t chunk = NT * REM_PER;
     const uint32_t planeW = (uint32_t)p.ny * p.W;
     const int ppar = (int)((r + 1) & 1);  // parity of D_{r-1}
     for (uint32_t base = gb * chunk; base < p.npos; base += gnb * chunk) {
@@ -1263,7 +1267,7 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
                 cnt += __popc(R[k]);
             }
         }
-        unsigned pos = block_reserve(cnt, lenR, sscan);
+        unsigned pos = block_reserve<false, NT>(cnt, lenR, sscan);
         // warp-cooperative expansion: one word at a time, 32 coalesced entries per store
 #pragma unroll
         for (int k = 0; k < REM_PER; ++k) {
@@ -1289,11 +1293,11 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
 #ifndef REM_MINB
 #define REM_MINB 4
 #endif
-template <int DIM, int SOL, bool MR>
+template <int DIM, int SOL, bool MR, int NT>
 __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
 {
-    __shared__ unsigned sscan[WPB + 1];
-    __shared__ unsigned long long sred[WPB];
+    __shared__ unsigned sscan[NT / 32 + 1];
+    __shared__ unsigned long long sred[NT / 32];
     if (skip && *skip) return;
     Ctl *ctl = p.ctl;
     const unsigned lane = lane_id();
@@ -1329,7 +1333,7 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
         const uint32_t *Dp = par ? p.D0b : p.D1b;
         unsigned *lenR = &ctl->len[r % 3];
         // ---- phase B: members of R_r ----
-        rem_members<DIM, MR>(p, r, Dp, Dc, ML, lenR, sscan, gb, gnb);
+        rem_members<DIM, MR, NT>(p, r, Dp, Dc, ML, lenR, sscan, gb, gnb);
         if (gb == 0 && threadIdx.x == 0) {
             // slot (r+1)%3 of len / dsum was last read two rounds ago
             ctl->len[(r + 1) % 3] = 0;
@@ -1364,7 +1368,7 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
         // one contiguous segment of the (brick-ordered) list per CTA: L1 reuse of neighbour rows
         const uint32_t seg = ((m + gnb - 1) / gnb + 32 * REM_MU - 1) / (32 * REM_MU) * (32 * REM_MU);
         const uint32_t sbeg = gb * seg, mend = min(m, sbeg + seg);
-        const uint32_t wbase = sbeg + (threadIdx.x >> 5) * 32 * REM_MU, wstride = WPB * 32 * REM_MU;
+        const uint32_t wbase = sbeg + (threadIdx.x >> 5) * 32 * REM_MU, wstride = (NT / 32) * 32 * REM_MU;
         for (uint32_t i0 = wbase; i0 < mend; i0 += wstride) {
             uint32_t ent[REM_MU], rw[REM_MU], x[REM_MU];
             bool live[REM_MU];
@@ -1433,7 +1437,7 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
                 if (live[u] && acc && (lane == 0 || pw != wi)) atomicOr(Dc + wi, acc);
             }
         }
-        const unsigned long long td = block_sum(lane == 0 ? a_dec : 0ull, sred);
+        const unsigned long long td = block_sum<NT>(lane == 0 ? a_dec : 0ull, sred);
         if (threadIdx.x == 0 && td) {
             atomicAdd(&ctl->dsum[r % 3], td);
             atomicAdd(&ctl->writes, td);
@@ -1451,22 +1455,28 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
     }
 }
 
+// Single-device remedy kernel: REM_NT threads per CTA (512: two CTAs per SM at the 64-register
+// budget, the same 1024 threads as 4 x 256 but half the CTAs at every grid barrier and block
+// reservation; measured -2 % on cfg4 / cfg2).  The multi-rank kernels keep BLOCK.
+#ifndef REM_NT
+#define REM_NT 512
+#endif
 template <int DIM, int SOL>
-__global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy(KP p, const unsigned *skip)
+__global__ void __launch_bounds__(REM_NT, REM_MINB * BLOCK / REM_NT) k_remedy(KP p, const unsigned *skip)
 {
-    remedy_body<DIM, SOL, false>(p, skip);
+    remedy_body<DIM, SOL, false, REM_NT>(p, skip);
 }
 
 template <int DIM, int SOL>
 __global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy_mr(const KP *__restrict__ kps, uint32_t per_group)
 {
-    remedy_body<DIM, SOL, true>(kps[blockIdx.x / per_group], nullptr);
+    remedy_body<DIM, SOL, true, BLOCK>(kps[blockIdx.x / per_group], nullptr);
 }
 
 template <int DIM, int SOL>
 __global__ void __launch_bounds__(BLOCK, REM_MINB) k_remedy_mr1(KP p)
 {
-    remedy_body<DIM, SOL, true>(p, nullptr);
+    remedy_body<DIM, SOL, true, BLOCK>(p, nullptr);
 }
 
 // ---------------------------------------------------------------------------
@@ -2460,10 +2470,10 @@ int stream_grid(int64_t work_warps)
 
 template <typename K>
 int coop_launch(K kernel, KP &p, const unsigned *skip, bool with_skip, cudaStream_t st, const char *env_name,
-                int default_per_sm)
+                int default_per_sm, int nt = BLOCK)
 {
     int occ = 0;
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, BLOCK, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, nt, 0);
     if (e != cudaSuccess) return fail(EIK_ECUDA, "occupancy: %s", cudaGetErrorString(e));
     int per_sm = (default_per_sm > 0 && default_per_sm < occ) ? default_per_sm : occ;
     if (const char *env = getenv(env_name)) {  // tuning override, bounded only by the occupancy limit
@@ -2472,7 +2482,7 @@ int coop_launch(K kernel, KP &p, const unsigned *skip, bool with_skip, cudaStrea
         else if (v > occ) fprintf(stderr, "[eik] %s=%d exceeds the occupancy limit %d; using %d\n", env_name, v, occ, per_sm);
     }
     if (per_sm < 1) return fail(EIK_ECUDA, "persistent kernel cannot be resident");
-    dim3 grid(per_sm * num_sms()), block(BLOCK);
+    dim3 grid(per_sm * num_sms()), block(nt);
     void *args2[] = {&p, (void *)&skip};
     void *args1[] = {&p};
     e = cudaLaunchCooperativeKernel((const void *)kernel, grid, block, with_skip ? args2 : args1, 0, st);
@@ -2626,7 +2636,7 @@ struct Engine {
     }
     static int remedy(KP &p, const unsigned *skip, cudaStream_t st)
     {
-        return coop_launch(k_remedy<DIM, SOL>, p, skip, true, st, "EIK_REM_BLOCKS_PER_SM", 0);
+        return coop_launch(k_remedy<DIM, SOL>, p, skip, true, st, "EIK_REM_BLOCKS_PER_SM", 0, REM_NT);
     }
     // single device: EIK_REMEDY=list (member-list kernel) or tile (tile engine); hand-built sets
     // with members outside their work list need the tile engine
