@@ -129,6 +129,10 @@ struct Ctl {
     alignas(128) unsigned bar_gen;  // multi-rank release generation
 #ifdef EIK_DIAG
     unsigned long long dg[4][26];   // remedy rounds by log2|R_r|: count, phase B ns, phase A ns, members
+    unsigned long long dgw[3][5];   // per round slot: max / sum of the CTAs' phase-B work ns, max / min start, max end
+    unsigned long long dg2[7][26];  // by log2|R_r|: sum of max-CTA B work, of mean-CTA B work, start skew, barrier tail,
+                                    // slowest CTA's members, rounds whose slowest CTA is CTA 0, its traversal share
+    unsigned long long dgk[3];      // per round slot: (B work ns << 24) | (members << 10) | CTA of the slowest CTA
     unsigned long long du[3][26];   // update iterations by log2|A_k|: count, ns, cells
 #endif
 };
@@ -1211,8 +1215,20 @@ __global__ void k_remedy_export(KP p, uint8_t *member)
 #ifndef REM_MU
 #define REM_MU 2            // phase A: members per lane in flight
 #endif
+// phase B: member words expanded per warp step.  2D: 4 (cfg2 remedy -6 %: a warp whose stretch
+// of the traversal is dense walks up to 128 words, and the slowest warp holds the grid barrier);
+// 3D: 1 (the extra registers spill in the 64-register list kernel and cost phase A more)
+#ifndef REM_XU2
+#define REM_XU2 4
+#endif
+#ifndef REM_XU3
+#define REM_XU3 1
+#endif
 
 
+#ifdef EIK_DIAG
+__shared__ unsigned dg_cta_members;
+#endif
 template <int DIM, bool MR, int NT>
 __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint32_t *__restrict__ Dp,
                                             uint32_t *Dc, uint32_t *ML, unsigned *lenR, unsigned *sscan, unsigned gb,
@@ -1268,7 +1284,12 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
             }
         }
         unsigned pos = block_reserve<false, NT>(cnt, lenR, sscan);
-        // warp-cooperative expansion: one word at a time, 32 coalesced entries per store
+#ifdef EIK_DIAG
+        if (cnt) atomicAdd(&dg_cta_members, cnt);
+#endif
+        // warp-cooperative expansion: one word at a time, 32 coalesced entries per store; XU words
+        // per step (their shuffles and stores are independent, so the steps overlap)
+        constexpr int XU = DIM == 2 ? REM_XU2 : REM_XU3;
 #pragma unroll
         for (int k = 0; k < REM_PER; ++k) {
             unsigned todo = __ballot_sync(FULL, R[k] != 0);
@@ -1276,14 +1297,23 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
             const uint32_t row = fdiv(w, p.fW);
             const uint32_t c0 = row * p.nx32 + (w - row * p.W) * 32u;
             while (todo) {
-                const int src = __ffs(todo) - 1;
-                todo &= todo - 1;
-                const uint32_t bits = __shfl_sync(FULL, R[k], src);
-                const uint32_t carry = __shfl_sync(FULL, C[k], src);
-                const uint32_t off = __shfl_sync(FULL, pos, src);
-                const uint32_t cc0 = __shfl_sync(FULL, c0, src);
-                if ((bits >> lane) & 1u)
-                    ML[off + __popc(bits & ((1u << lane) - 1u))] = (cc0 + lane) | (((carry >> lane) & 1u) ? CARRY : 0u);
+                int src[XU];
+                bool has[XU];
+#pragma unroll
+                for (int q = 0; q < XU; ++q) {
+                    has[q] = todo != 0;
+                    src[q] = has[q] ? __ffs(todo) - 1 : 0;
+                    todo &= todo - 1;
+                }
+#pragma unroll
+                for (int q = 0; q < XU; ++q) {
+                    const uint32_t bits = __shfl_sync(FULL, R[k], src[q]);
+                    const uint32_t carry = __shfl_sync(FULL, C[k], src[q]);
+                    const uint32_t off = __shfl_sync(FULL, pos, src[q]);
+                    const uint32_t cc0 = __shfl_sync(FULL, c0, src[q]);
+                    if (has[q] && ((bits >> lane) & 1u))
+                        ML[off + __popc(bits & ((1u << lane) - 1u))] = (cc0 + lane) | (((carry >> lane) & 1u) ? CARRY : 0u);
+                }
             }
             pos += __popc(R[k]);
         }
@@ -1322,9 +1352,14 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
     for (int64_t rr = p.it0; rr < p.it0 + p.max_it; ++rr) {
         const uint32_t r = (uint32_t)rr;
 #ifdef EIK_DIAG
-        unsigned long long dgt0 = 0, dgt1 = 0;
+        unsigned long long dgt0 = 0, dgt1 = 0, dgc0 = 0;
         int dgb = 0;
         if (lead) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dgt0));
+        if (threadIdx.x == 0) {
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dgc0));
+            dg_cta_members = 0;
+        }
+        __syncthreads();
 #endif
         const int par = (int)(r & 1);
         const real_t *__restrict__ Pc = par ? p.P1 : p.P0;
@@ -1338,7 +1373,24 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
             // slot (r+1)%3 of len / dsum was last read two rounds ago
             ctl->len[(r + 1) % 3] = 0;
             ctl->dsum[(r + 1) % 3] = 0;
+#ifdef EIK_DIAG
+            for (int q = 0; q < 5; ++q) ctl->dgw[(r + 1) % 3][q] = q == 3 ? ~0ull : 0ull;
+            ctl->dgk[(r + 1) % 3] = 0;
+#endif
         }
+#ifdef EIK_DIAG
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long dgc1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(dgc1));
+            atomicMax(&ctl->dgw[r % 3][0], dgc1 - dgc0);
+            atomicAdd(&ctl->dgw[r % 3][1], dgc1 - dgc0);
+            atomicMax(&ctl->dgw[r % 3][2], dgc0);
+            atomicMin(&ctl->dgw[r % 3][3], dgc0);
+            atomicMax(&ctl->dgw[r % 3][4], dgc1);
+            atomicMax(&ctl->dgk[r % 3], ((dgc1 - dgc0) << 24) | ((unsigned long long)min(dg_cta_members, 16383u) << 10) | gb);
+        }
+#endif
         if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
         const unsigned m = vload(lenR);  // this rank's |R_r| (list length)
         const unsigned long long mg = MR ? ranks_len<MR>(p, (int)(r % 3)) : m;  // global |R_r|
@@ -1361,6 +1413,14 @@ __device__ __forceinline__ void remedy_body(const KP &p, const unsigned *skip)
             ctl->dg[0][dgb] += 1;
             ctl->dg[1][dgb] += dgt1 - dgt0;
             ctl->dg[3][dgb] += mg;
+            ctl->dg2[0][dgb] += ctl->dgw[r % 3][0];
+            ctl->dg2[1][dgb] += ctl->dgw[r % 3][1] / gnb;
+            ctl->dg2[2][dgb] += ctl->dgw[r % 3][2] - ctl->dgw[r % 3][3];
+            ctl->dg2[3][dgb] += dgt1 > ctl->dgw[r % 3][4] ? dgt1 - ctl->dgw[r % 3][4] : 0ull;
+            const unsigned long long kk = ctl->dgk[r % 3];
+            ctl->dg2[4][dgb] += (kk >> 10) & 16383u;
+            ctl->dg2[5][dgb] += (kk & 1023u) == 0u;
+            ctl->dg2[6][dgb] += kk & 1023u;
 #endif
         }
         // ---- phase A: one local solve per member, REM_MU members per lane in flight ----
@@ -3069,6 +3129,16 @@ int EIK_FN(eik_ifim_solve)(const eik_geom *g, real_t *phi, const real_t *speed, 
                 fprintf(stderr, "[eik diag] |R|~2^%2d rounds %6llu members %12llu  B %9.3f ms  A %9.3f ms  (%.2f/%.2f us per round)\n",
                         k, c[1].dg[0][k], c[1].dg[3][k], c[1].dg[1][k] * 1e-6, c[1].dg[2][k] * 1e-6,
                         c[1].dg[1][k] * 1e-3 / c[1].dg[0][k], c[1].dg[2][k] * 1e-3 / c[1].dg[0][k]);
+        for (int k = 0; k < 26; ++k)
+            if (c[1].dg[0][k])
+                fprintf(stderr, "[eik diag] |R|~2^%2d phase B per round: slowest CTA %.2f us, mean CTA %.2f us, start skew %.2f us, last arrival -> lead release %.2f us\n",
+                        k, c[1].dg2[0][k] * 1e-3 / c[1].dg[0][k], c[1].dg2[1][k] * 1e-3 / c[1].dg[0][k],
+                        c[1].dg2[2][k] * 1e-3 / c[1].dg[0][k], c[1].dg2[3][k] * 1e-3 / c[1].dg[0][k]);
+        for (int k = 0; k < 26; ++k)
+            if (c[1].dg[0][k])
+                fprintf(stderr, "[eik diag] |R|~2^%2d slowest CTA: %.0f members (mean %.0f per CTA), CTA 0 in %llu of %llu rounds, mean id %.1f\n",
+                        k, (double)c[1].dg2[4][k] / c[1].dg[0][k], (double)c[1].dg[3][k] / c[1].dg[0][k] / 296.0,
+                        c[1].dg2[5][k], c[1].dg[0][k], (double)c[1].dg2[6][k] / c[1].dg[0][k]);
     }
 #endif
     if (history && history_cap > 0 && c[0].iters > 0) {
