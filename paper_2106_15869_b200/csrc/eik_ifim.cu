@@ -134,6 +134,8 @@ struct Ctl {
                                     // slowest CTA's members, rounds whose slowest CTA is CTA 0, its traversal share
     unsigned long long dgk[3];      // per round slot: (B work ns << 24) | (members << 10) | CTA of the slowest CTA
     unsigned long long du[3][26];   // update iterations by log2|A_k|: count, ns, cells
+    unsigned long long duw[3][2];   // per iteration slot: max / sum of the CTAs' work ns (start -> arrival)
+    unsigned long long du2[2][26];  // by log2|A_k|: sum of slowest-CTA work, of mean-CTA work
 #endif
 };
 
@@ -908,6 +910,10 @@ __device__ __forceinline__ void update_body(const KP &p)
     uint32_t pre = 0;
     bool have_pre = false;
     for (int64_t it = p.it0; it < p.it0 + p.max_it; ++it) {
+#ifdef EIK_DIAG
+        unsigned long long duc0 = 0;
+        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(duc0));
+#endif
         const int par = (int)(it & 1);
         const real_t *__restrict__ Pc = par ? p.P1 : p.P0;
         real_t *__restrict__ Pn = par ? p.P0 : p.P1;
@@ -1034,7 +1040,19 @@ __device__ __forceinline__ void update_body(const KP &p)
         }
         if (gb == 0 && threadIdx.x == 0) {
             ctl->len[(it + 2) % 3] = 0;
+#ifdef EIK_DIAG
+            ctl->duw[(it + 1) % 3][0] = ctl->duw[(it + 1) % 3][1] = 0;
+#endif
         }
+#ifdef EIK_DIAG
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long duc1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(duc1));
+            atomicMax(&ctl->duw[it % 3][0], duc1 - duc0);
+            atomicAdd(&ctl->duw[it % 3][1], duc1 - duc0);
+        }
+#endif
         if (!grid_barrier_n(ctl, gnb, MR ? &p : nullptr)) return;
         if (UPD_PREF && !MR) {
             const unsigned i0 = gb * (BLOCK * UPD_MU) + threadIdx.x;
@@ -1052,6 +1070,8 @@ __device__ __forceinline__ void update_body(const KP &p)
                 ctl->du[0][bk] += 1;
                 ctl->du[1][bk] += tnow - ctl->du[2][25];
                 ctl->du[2][bk] += n;
+                ctl->du2[0][bk] += ctl->duw[it % 3][0];
+                ctl->du2[1][bk] += ctl->duw[it % 3][1] / gnb;
             }
             ctl->du[2][25] = tnow;  // last barrier time (bucket 25 of cells is never reached)
         }
@@ -3124,6 +3144,10 @@ int EIK_FN(eik_ifim_solve)(const eik_geom *g, real_t *phi, const real_t *speed, 
             if (c[0].du[0][k])
                 fprintf(stderr, "[eik diag] update |A|~2^%2d iterations %6llu cells %12llu  %9.3f ms  (%.2f us per iteration)\n",
                         k, c[0].du[0][k], c[0].du[2][k], c[0].du[1][k] * 1e-6, c[0].du[1][k] * 1e-3 / c[0].du[0][k]);
+        for (int k = 0; k < 25; ++k)
+            if (c[0].du[0][k])
+                fprintf(stderr, "[eik diag] update |A|~2^%2d per iteration: slowest CTA %.2f us, mean CTA %.2f us\n", k,
+                        c[0].du2[0][k] * 1e-3 / c[0].du[0][k], c[0].du2[1][k] * 1e-3 / c[0].du[0][k]);
         for (int k = 0; k < 26; ++k)
             if (c[1].dg[0][k])
                 fprintf(stderr, "[eik diag] |R|~2^%2d rounds %6llu members %12llu  B %9.3f ms  A %9.3f ms  (%.2f/%.2f us per round)\n",
