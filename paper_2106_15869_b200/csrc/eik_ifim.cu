@@ -1241,6 +1241,18 @@ __global__ void k_remedy_export(KP p, uint8_t *member)
 #ifndef REM_XU2
 #define REM_XU2 4
 #endif
+// 3D phase B: member expansion through per-warp shared-memory staging (cfg4 remedy 263.0 ->
+// 257.5 ms, cfg3 4.30 -> 4.15 ms); 2D: REM_STAGE2 (the shuffle form with REM_XU2 words per step
+// is the default there)
+#ifndef REM_STAGE
+#define REM_STAGE 1
+#endif
+#ifndef REM_STAGE2
+#define REM_STAGE2 0
+#endif
+#ifndef REM_SXU
+#define REM_SXU 2
+#endif
 #ifndef REM_XU3
 #define REM_XU3 1
 #endif
@@ -1310,6 +1322,37 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
         // warp-cooperative expansion: one word at a time, 32 coalesced entries per store; XU words
         // per step (their shuffles and stores are independent, so the steps overlap)
         constexpr int XU = DIM == 2 ? REM_XU2 : REM_XU3;
+        if (DIM == 3 ? REM_STAGE : REM_STAGE2) {
+            // each warp stages its member words of step k in shared memory ({bits, carry,
+            // first cell, first slot}) and walks them with broadcast loads, REM_SXU per step: no
+            // shuffles, and the unrolled walk needs no per-word registers beyond the entry
+            __shared__ uint4 s_q[NT / 32][32];
+            const unsigned warp = threadIdx.x >> 5;
+            const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+            for (int k = 0; k < REM_PER; ++k) {
+                const unsigned m = __ballot_sync(FULL, R[k] != 0);
+                if (R[k]) {
+                    const uint32_t row = fdiv(WW[k], p.fW);
+                    s_q[warp][__popc(m & lt)] = make_uint4(R[k], C[k], row * p.nx32 + (WW[k] - row * p.W) * 32u, pos);
+                }
+                pos += __popc(R[k]);
+                __syncwarp();
+                const int n = __popc(m);
+                for (int j = 0; j < n; j += REM_SXU) {
+#pragma unroll
+                    for (int q = 0; q < REM_SXU; ++q) {
+                        if (j + q < n) {
+                            const uint4 e = s_q[warp][j + q];
+                            if ((e.x >> lane) & 1u)
+                                ML[e.w + __popc(e.x & lt)] = (e.z + lane) | (((e.y >> lane) & 1u) ? CARRY : 0u);
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+            continue;
+        }
 #pragma unroll
         for (int k = 0; k < REM_PER; ++k) {
             unsigned todo = __ballot_sync(FULL, R[k] != 0);
