@@ -1351,8 +1351,7 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
                 }
                 __syncwarp();
             }
-            continue;
-        }
+        } else {
 #pragma unroll
         for (int k = 0; k < REM_PER; ++k) {
             unsigned todo = __ballot_sync(FULL, R[k] != 0);
@@ -1379,6 +1378,7 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
                 }
             }
             pos += __popc(R[k]);
+        }
         }
     }
 }
