@@ -1241,17 +1241,20 @@ __global__ void k_remedy_export(KP p, uint8_t *member)
 #ifndef REM_XU2
 #define REM_XU2 4
 #endif
-// 3D phase B: member expansion through per-warp shared-memory staging (cfg4 remedy 263.0 ->
-// 257.5 ms, cfg3 4.30 -> 4.15 ms); 2D: REM_STAGE2 (the shuffle form with REM_XU2 words per step
-// is the default there)
+// Phase B member expansion through per-warp shared-memory staging (3D: cfg4 remedy 263.0 ->
+// 257.5 ms, cfg3 4.30 -> 4.15 ms; 2D with 8 words per step: cfg2 49.6 -> 48.4 ms against the
+// shuffle form with REM_XU2 words per step, which REM_STAGE / REM_STAGE2 = 0 select)
 #ifndef REM_STAGE
 #define REM_STAGE 1
 #endif
 #ifndef REM_STAGE2
-#define REM_STAGE2 0
+#define REM_STAGE2 1
 #endif
 #ifndef REM_SXU
-#define REM_SXU 2
+#define REM_SXU 2   // staged words walked per step, 3D
+#endif
+#ifndef REM_SXU2
+#define REM_SXU2 8  // staged words walked per step, 2D
 #endif
 #ifndef REM_XU3
 #define REM_XU3 1
@@ -1339,9 +1342,10 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
                 pos += __popc(R[k]);
                 __syncwarp();
                 const int n = __popc(m);
-                for (int j = 0; j < n; j += REM_SXU) {
+                constexpr int SXU = DIM == 2 ? REM_SXU2 : REM_SXU;
+                for (int j = 0; j < n; j += SXU) {
 #pragma unroll
-                    for (int q = 0; q < REM_SXU; ++q) {
+                    for (int q = 0; q < SXU; ++q) {
                         if (j + q < n) {
                             const uint4 e = s_q[warp][j + q];
                             if ((e.x >> lane) & 1u)
