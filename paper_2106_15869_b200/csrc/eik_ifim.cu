@@ -1257,6 +1257,14 @@ __global__ void k_remedy_export(KP p, uint8_t *member)
 #ifndef REM_CSTAGE2
 #define REM_CSTAGE2 1
 #endif
+// Phase B work assignment: 0 = each CTA takes NT*REM_PER consecutive traversal positions per
+// sweep; 1 = consecutive 32*REM_PER-position warp blocks go to different CTAs
+#ifndef REM_WIL2
+#define REM_WIL2 1
+#endif
+#ifndef REM_WIL3
+#define REM_WIL3 2
+#endif
 #ifndef REM_CSTAGE3
 #define REM_CSTAGE3 1
 #endif
@@ -1286,12 +1294,26 @@ __device__ __forceinline__ void rem_members(const KP &p, uint32_t r, const uint3
     const uint32_t chunk = NT * REM_PER;
     const uint32_t planeW = (uint32_t)p.ny * p.W;
     const int ppar = (int)((r + 1) & 1);  // parity of D_{r-1}
-    for (uint32_t base = gb * chunk; base < p.npos; base += gnb * chunk) {
+    // 3D (REM_WIL3 = 2): interleave only when one sweep covers the grid; with several sweeps the
+    // strided chunks already spread a front over the CTAs and contiguous chunks keep phase A's
+    // list segments local
+    const bool WIL = DIM == 2 ? REM_WIL2 != 0 : (REM_WIL3 == 1 || (REM_WIL3 == 2 && p.npos <= gnb * chunk));
+    const uint32_t wchunk = 32u * REM_PER, wrp = threadIdx.x >> 5;
+    for (uint32_t it = 0;; ++it) {
+        uint32_t pbase;  // this thread's first traversal position
+        if (WIL) {
+            if (((it * (NT / 32)) * gnb + gb) * wchunk >= p.npos) break;  // warp 0 holds the CTA's lowest block
+            pbase = ((it * (NT / 32) + wrp) * gnb + gb) * wchunk + lane * REM_PER;
+        } else {
+            const uint32_t base = (gb + it * gnb) * chunk;
+            if (base >= p.npos) break;
+            pbase = base + threadIdx.x * REM_PER;
+        }
         uint32_t R[REM_PER], C[REM_PER], WW[REM_PER];
         unsigned cnt = 0;
 #pragma unroll
         for (int k = 0; k < REM_PER; ++k) {
-            const uint32_t w = word_at<DIM>(p, base + threadIdx.x * REM_PER + k);  // brick order (see word_at)
+            const uint32_t w = pbase + k < p.npos ? word_at<DIM>(p, pbase + k) : 0xffffffffu;  // brick order (see word_at)
             WW[k] = w;
             R[k] = C[k] = 0;
             if (w < p.nwords) {
